@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the Tiny-Twin channel convolution hot path (BASELINE.json metric:
+channel-convolved complex samples/s for the whole box, real-time UE count, %
+roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+
+Workload (default c4, BASELINE.json configs[3]: 512 UEs x DL/UL, 48 taps in
+[0, 1024], snapshots every 256 samples, 10 dB AWGN, 0.5 ms slots of 61,440
+samples at 122.88 Msps, "sharded across 1/2/4/8 GPUs"). One step = one slot: one
+`tt_channel_apply` over every channel this rank owns, with the delay line carried
+from the previous slot. UEs are sharded in contiguous blocks over ranks (no
+collective on the data path; NCCL only for the barrier and the max-over-ranks
+timing). Inputs are synthetic (ttsynth) and resident in HBM before timing; a
+rotating pool of distinct slot buffers totalling >= 4x L2 is cycled so no step's
+input is L2-resident. See DESIGN.md §6 for the roofline and metric definitions.
+
+Under torchrun every rank runs its shard; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import ttsynth  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+SM_COUNT_NOMINAL = 148
+FP32_LANES_PER_SM = 128  # FFMA lanes per SM per clock (2 flop each)
+
+
+def _peaks():
+    p = {"hbm_gbs": 6549.8, "sm_max_mhz": 1965.0, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update(hbm_gbs=float(m["hbm_gbs"]), sm_max_mhz=float(m.get("sm_max_mhz", 1965.0)), source="measured")
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake_slowdown": 0x80}
+    NOTE = {"sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                self.reasons |= int(self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if self._nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [k for k, v in {**self.BAD, **self.NOTE}.items() if self.reasons & v]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def roofline(w: ttsynth.Workload, samples: int, kernel_s: float, peaks: dict, traffic):
+    """NS roofline: min(HBM / 16 B per sample, FP32 / 8L flop per sample) per GPU."""
+    fp32 = SM_COUNT_NOMINAL * FP32_LANES_PER_SM * 2 * peaks["sm_max_mhz"] * 1e6  # flop/s
+    hbm = peaks["hbm_gbs"] * 1e9                                                # B/s
+    hbm_rate, alu_rate = hbm / 16.0, fp32 / (8.0 * w.L)
+    if alu_rate < hbm_rate:
+        achieved = 8.0 * w.L * samples / kernel_s / 1e12
+        rl = {"bound": "alu", "achieved": achieved, "peak": fp32 / 1e12, "unit": "TFLOP/s"}
+    else:
+        achieved = 16.0 * samples / kernel_s / 1e9
+        rl = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    rl["frac"] = rl["achieved"] / rl["peak"]
+    rl["traffic"] = traffic
+    rl["peak_source"] = peaks["source"] + (" (FP32 peak = 148 SM x 128 lanes x 2 x sm_max_mhz)"
+                                           if rl["bound"] == "alu" else " (MEASURED_PEAKS.json hbm_gbs)")
+    rl["ns_samples_per_s_per_gpu"] = min(hbm_rate, alu_rate)
+    return rl
+
+
+def _traffic(config: str):
+    """dram read+write bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(w: ttsynth.Workload, target_s: float = 10.0):
+    """The oracle (as it stands) on this host's cores, on a bounded sample of the
+    workload: whole slots of the first channels, grown until ~target_s of wall time."""
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    n = w.n_per_call
+    chans, elapsed, done = 1, 0.0, 0
+    d_all = ttsynth.delays(w, 0, min(w.C, 4096))
+    while True:
+        c = min(chans, w.C)
+        K = (n - 1) // w.S + 2
+        g = ttsynth.snapshots(w, 0, c, K)
+        x = ttsynth.iq(w, 0, c, 0)
+        t0 = time.perf_counter()
+        oracle.convolve(d_all[:c], w.S, g, 0, x, 0, 0, n, sigma=w.sigma, seed=0)
+        dt = time.perf_counter() - t0
+        elapsed, done = dt, c * n
+        if dt >= target_s / 4 or c >= w.C or c >= 4096:
+            break
+        chans = min(w.C, max(c * 2, int(c * target_s / max(dt, 1e-3))))
+    return {"value": done / elapsed, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{min(chans, w.C)} channels x 1 slot of {n} samples of {w.name} "
+                      f"({done} samples, {elapsed:.2f} s wall, double precision, OpenMP)"}
+
+
+def run_reference(args, w):
+    """--impl reference: the oracle timed as the reference arm, rank 0 only."""
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    # each step: one slot of a bounded channel sample, sized for ~2 s per step
+    n = w.n_per_call
+    K = (n - 1) // w.S + 2
+    c = 1
+    g = ttsynth.snapshots(w, 0, 64, K)
+    x = ttsynth.iq(w, 0, 64, 0)
+    d = ttsynth.delays(w, 0, 64)
+    t0 = time.perf_counter()
+    oracle.convolve(d[:1], w.S, g[:1], 0, x[:1], 0, 0, n, sigma=w.sigma)
+    one = time.perf_counter() - t0
+    c = int(max(1, min(64, 2.0 / max(one, 1e-4))))
+    for _ in range(args.warmup):
+        oracle.convolve(d[:c], w.S, g[:c], 0, x[:c], 0, 0, n, sigma=w.sigma)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.convolve(d[:c], w.S, g[:c], 0, x[:c], 0, 0, n, sigma=w.sigma)
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    val = c * n * args.steps / tot
+    line = {
+        "impl": "reference", "metric": "channel-convolved complex samples/s (whole box)", "value": val,
+        "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(w, world),
+        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{c} of {w.C} channels x 1 slot of {n} samples per step"},
+        "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "realtime_ues": w.realtime_ues(val),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config(w, world):
+    return {"workload": f"BASELINE configs {w.name}", "ues": w.ues, "channels": w.C,
+            "channels_per_ue": w.dirs, "samples_per_call": w.n_per_call, "taps": w.L, "max_delay": w.D,
+            "snapshot_period": w.S, "snr_db": w.snr_db, "sample_rate_sps": w.rate_sps,
+            "parallelism": f"ue-shard x{world}",
+            "l2": "rotating pool of distinct slot inputs, >= 4x L2 per rank (inputs not L2-resident)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    w = ttsynth.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, w)
+        return
+
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    rank, world, local = _dist()
+    if world != args.gpus and rank == 0:
+        print(f"note: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    # ---- this rank's shard (contiguous UE block; DL/UL of a UE stay together) ----------
+    c_lo, c_hi = ttsynth.shard_ues(w, rank, world)
+    C, n = c_hi - c_lo, w.n_per_call
+    steps_total = args.warmup + args.steps
+    K = (steps_total * n - 1) // w.S + 2
+    delays = ttsynth.delays(w, c_lo, c_hi)
+    gains = ttsynth.snapshots(w, c_lo, c_hi, K, backend="torch", device=dev)
+    slot_bytes = C * n * 8
+    P = max(2, math.ceil(4 * L2_BYTES / max(slot_bytes, 1)))
+    P = min(P, steps_total)
+    xs = [ttsynth.iq(w, c_lo, c_hi, i, backend="torch", device=dev) for i in range(P)]
+    y = torch.empty_like(xs[0])
+    ch = Channel(delays, w.S, seed=12345, snapshot_capacity=K, channel_offset=c_lo, device=dev)
+    ch.load_snapshots(gains, 0)
+    del gains
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    sigma = w.sigma
+
+    # ---- device-resident timed region ----------------------------------------------
+    for i in range(args.warmup):
+        ch.apply(xs[i % P], out=y, noise_sigma=sigma)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            ch.apply(xs[(args.warmup + i) % P], out=y, noise_sigma=sigma)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]  # ms, one launch each
+    elapsed_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    elapsed_max = float(t.item())
+    samples_all = w.C * n * args.steps  # every rank's channels
+    value = samples_all / (elapsed_max / 1e3)
+    kernel_s = statistics.mean(per_step) / 1e3
+
+    # ---- end-to-end through the C ABI with host buffers (H2D + D2H inside) -----------
+    e2e = None
+    if args.e2e_steps > 0:
+        xh = [xs[i % P].cpu().pin_memory() for i in range(min(P, 2))]
+        yh = torch.empty_like(xh[0]).pin_memory()
+        ch.apply_host(xh[0], yh, noise_sigma=sigma)  # staging allocation + warm-up
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.e2e_steps):
+            ch.apply_host(xh[i % len(xh)], yh, noise_sigma=sigma)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if pg:
+            pg.all_reduce(te, op=pg.ReduceOp.MAX)
+        e2e = {"value": w.C * n * args.e2e_steps / (float(te.item()) / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": slot_bytes, "d2h_bytes_per_step": slot_bytes,
+               "steps": args.e2e_steps, "api": "tt_channel_apply_host (pinned host buffers)"}
+    info = ch.info()
+    ch.close()
+
+    if rank == 0:
+        peaks = _peaks()
+        rl = roofline(w, C * n, kernel_s, peaks, _traffic(w.name))
+        line = {
+            "metric": "channel-convolved complex samples/s (whole box)",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _config(w, world),
+            "roofline": rl,
+            "realtime_ues": w.realtime_ues(value),
+            "ns_fraction_box": value / (world * rl["ns_samples_per_s_per_gpu"]),
+            "call_ms": {"p50": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
+                        "slot_ms": 1e3 * n / w.rate_sps},
+            "gpu_launches": args.steps * int(info.launches_per_apply),
+            "plan": {"outputs_per_thread": int(info.outputs_per_thread), "threads_per_cta": 256},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(w)
+        elif not args.no_cpu_baseline:
+            line["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": len(os.sched_getaffinity(0)),
+                                    "kind": "oracle", "sample": "reported at N=1 only"}
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,159 @@
+/*
+ * tt_channel.h — C ABI of the B200-native Tiny-Twin channel convolution
+ * (arXiv 2601.08217). This is the boundary of the hot path: the Python binding
+ * (paper_2601_08217_b200/_lib.py), the tests and bench.py call exactly these
+ * functions; every arithmetic step runs in the library's sm_100a kernels.
+ *
+ * Citations: "P:<n>" = PAPER.md line n; "S:<n>" = SPEC.md line n; "NS" =
+ * BASELINE.json north_star; "R<k>" = reading k of the paper in DESIGN.md §3.
+ *
+ * What one handle computes (NS formula; §III-B "y_u(t) = x(t) * h_u(t)
+ * ... the convolution operator * denotes linear convolution and varies
+ * independently for each receiver"; §III-B "time-varying CIR traces ...
+ * per-UE linear filtering"; §IV "discrete complex tap values over time ...
+ * on a fixed delay grid"):
+ *
+ *   for every channel c of the handle and every global sample n of its stream
+ *   (n counts from create/reset across all apply calls):
+ *     k = floor(n / S), alpha = (n - k S) / S
+ *     h_{c,l}[n] = g_{c,l,k} + alpha (g_{c,l,k+1} - g_{c,l,k})       (R1, R2)
+ *     y_c[n] = sum_l h_{c,l}[n] x_c[n - d_{c,l}] + w_c[n],  x_c[m] = 0 for m < 0 (R4)
+ *
+ * with w_c[n] the AWGN of docs/tt-normal-v1.md keyed by (seed, channel_offset + c,
+ * n). Arithmetic is float32 (FMA); taps are summed in ascending-delay order (ties
+ * by tap index), so a channel's outputs are bit-identical for any split of its
+ * stream into apply calls, any channel grouping and any GPU count.
+ *
+ * Data layout (all row-major, interleaved complex float32 = (re, im) pairs):
+ *   delays  int32 [C][L]                  (host)
+ *   gains   float [C][count][L][2]        (host or device)
+ *   in/out  float [C][n_samples][2]       (device for tt_channel_apply,
+ *                                           host for tt_channel_apply_host)
+ * "UE" in this API means one directional channel stream: a UE's DL and UL are
+ * two channels (c = 2u + dir), as in P:330's UE-localised DL+UL convolution.
+ *
+ * Errors: every call returns a tt_status and never aborts or prints; the
+ * thread-local message of the last failure is tt_last_error(). A failed call
+ * leaves the handle unchanged (apply: t is not advanced).
+ * Threading: a handle is not thread-safe; calls on one handle must be
+ * stream-ordered (use one stream per handle, or order them yourself).
+ */
+#ifndef TT_CHANNEL_H
+#define TT_CHANNEL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_ABI_VERSION 1
+#define TT_MAX_DELAY 4096  /* delays are integers in [0, TT_MAX_DELAY] (R5) */
+#define TT_MAX_TAPS 4096
+
+typedef struct tt_channel_s* tt_channel_t; /* opaque; owned by the library */
+typedef void* tt_stream_t;                 /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+    TT_OK = 0,
+    TT_ERR_INVALID_ARG = 1,      /* bad size, pointer, delay, period or sigma */
+    TT_ERR_OUT_OF_MEMORY = 2,    /* a device or pinned allocation failed */
+    TT_ERR_CUDA = 3,             /* a CUDA runtime call or launch failed (see tt_last_error) */
+    TT_ERR_SNAPSHOT_MISSING = 4, /* apply needs a snapshot index that is not resident */
+    TT_ERR_UNSUPPORTED = 5       /* e.g. no sm_100 device */
+} tt_status;
+
+typedef struct {
+    int32_t num_ue;            /* C: channel streams in this handle */
+    int32_t num_taps;          /* L */
+    int32_t snapshot_period;   /* S */
+    int32_t history;           /* H: delay-line samples kept per channel (max delay rounded up to even) */
+    int32_t max_delay;         /* max over all d_{c,l} */
+    int32_t device;            /* CUDA device the handle is bound to */
+    int64_t t;                 /* global index of the next sample to be applied */
+    int64_t snapshot_capacity; /* ring slots per channel */
+    int64_t resident_lo;       /* resident snapshot indices are [resident_lo, resident_hi) */
+    int64_t resident_hi;
+    int64_t channel_offset;    /* global id of channel 0 (noise key) */
+    uint64_t seed;             /* noise key */
+    int64_t device_bytes;      /* device memory owned by the handle */
+    int32_t outputs_per_thread; /* tiled-kernel plan R (T = 256 R outputs per tile); 0 = generic kernel */
+    int32_t launches_per_apply; /* kernel launches one tt_channel_apply enqueues */
+} tt_channel_info;
+
+/* Create a handle for C = num_ue channels with L = num_taps taps each.
+ *   delays: host int32 [C][L], each in [0, TT_MAX_DELAY]; duplicates allowed (the
+ *     taps add, R6). The library copies them.
+ *   snapshot_period: S >= 1 samples between gain snapshots (P:411's trace time step,
+ *     R2); snapshot k is the gain at global sample k S.
+ *   seed: noise key (docs/tt-normal-v1.md).
+ *   snapshot_capacity: snapshot slots per channel kept on the device (>= 2); a ring.
+ *   channel_offset: global id of this handle's channel 0 (so a sharded run keys
+ *     noise by global channel, NS "keyed by (seed, UE, sample)").
+ * Binds to the current CUDA device. Allocates: the ring C x capacity x L x 8 B, the
+ * delay-line history 2 x C x H x 8 B, and small per-channel tables; zeroes the
+ * history (R4) and sets t = 0.
+ * Errors: INVALID_ARG (out == NULL, C <= 0, L <= 0 or > TT_MAX_TAPS, delays == NULL,
+ *   a delay outside [0, TT_MAX_DELAY], S <= 0, capacity < 2, channel_offset < 0),
+ *   UNSUPPORTED (current device is not compute capability 10.x), OUT_OF_MEMORY, CUDA. */
+tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps, const int32_t* delays,
+                            int32_t snapshot_period, uint64_t seed, int64_t snapshot_capacity,
+                            int64_t channel_offset);
+
+/* Load gain snapshots first_index .. first_index+count-1 of every channel
+ * ("read time-varying CIR traces"; "discrete complex tap values over
+ * time") into the ring. gains: float [C][count][L][2], host or device memory (the
+ * library detects which); the copy is enqueued on `stream` and the source must stay
+ * valid until it completes there. If the new block is contiguous with the resident
+ * range the range grows (older snapshots fall out once capacity is exceeded);
+ * otherwise the resident range is replaced by the new block.
+ * Errors: INVALID_ARG (NULL handle/gains, first_index < 0, count <= 0,
+ *   count > capacity), CUDA. */
+tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t first_index, int64_t count,
+                                    tt_stream_t stream);
+
+/* Apply the channel to the next n_samples samples of every channel's stream:
+ * in/out: device float [C][n_samples][2]; in and out must not overlap. One kernel
+ * launch on `stream`; no synchronisation, no allocation. Carries the delay line:
+ * y of this call uses the last H input samples of the previous calls (zeros at
+ * stream start), "ConvState ... carried tail". noise_sigma: complex
+ * standard deviation of the AWGN (E|w|^2 = sigma^2); 0 = no noise (R8).
+ * Needs snapshots floor(t/S) .. floor((t+n_samples-1)/S)+1 resident (R3).
+ * On success t += n_samples.
+ * Errors: INVALID_ARG (NULL handle/in/out, n_samples <= 0, in == out, sigma < 0 or
+ *   not finite), SNAPSHOT_MISSING, CUDA (launch failure). */
+tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
+                           tt_stream_t stream);
+
+/* Same as tt_channel_apply but `in` and `out` are HOST memory (pinned for full
+ * overlap; pageable works but copies synchronously). The library pipelines
+ * host->device copies, the kernel and device->host copies over channel chunks on
+ * internal streams ordered after / before `stream`; out is complete when `stream`
+ * reaches this point. Lazily allocates device staging (3 chunk buffers) on first use
+ * or growth. Errors: as tt_channel_apply, plus OUT_OF_MEMORY. */
+tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
+                                tt_stream_t stream);
+
+/* t = 0 and zero delay-line history (stream-ordered on `stream`); the resident
+ * snapshot range is kept. Errors: INVALID_ARG, CUDA. */
+tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream);
+
+/* Fill *info. Errors: INVALID_ARG. */
+tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info);
+
+/* Synchronise the handle's device, free everything the handle owns. NULL is OK. */
+tt_status tt_channel_destroy(tt_channel_t h);
+
+/* Thread-local message describing the last failed call on this thread ("" if none). */
+const char* tt_last_error(void);
+
+/* Static name of a status code. */
+const char* tt_status_string(tt_status s);
+
+/* TT_ABI_VERSION the library was built with. */
+int32_t tt_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_CHANNEL_H */

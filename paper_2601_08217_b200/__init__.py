@@ -1,0 +1,18 @@
+"""B200-native Tiny-Twin channel convolution (arXiv 2601.08217).
+
+The hot path is the C-ABI library libtt.so (include/tt_channel.h) built from
+csrc/ for sm_100a; `_lib` marshals arguments to it and `Channel` wraps a handle
+with torch tensors. There is no CPU fallback: importing works without a GPU, but
+every compute call goes through the CUDA library.
+"""
+from ._lib import TTError, tt_abi_version  # noqa: F401
+
+__all__ = ["Channel", "TTError", "tt_abi_version"]
+
+
+def __getattr__(name):
+    if name == "Channel":  # torch is imported lazily
+        from .channel import Channel
+
+        return Channel
+    raise AttributeError(name)

@@ -1,0 +1,118 @@
+"""`Channel`: a thin torch-facing wrapper over one tt_channel handle.
+
+PyTorch supplies device memory and streams only; every sample is computed by the
+library's kernels (see include/tt_channel.h for semantics and errors).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Channel:
+    """C = num_ue channel streams with L taps at integer delays (host [C][L])."""
+
+    def __init__(self, delays, snapshot_period: int, seed: int = 0, snapshot_capacity: int = 2,
+                 channel_offset: int = 0, device: Optional[torch.device] = None):
+        d = np.ascontiguousarray(np.asarray(delays, dtype=np.int32))
+        if d.ndim != 2:
+            raise ValueError("delays must be [C][L]")
+        self.C, self.L = int(d.shape[0]), int(d.shape[1])
+        self.S = int(snapshot_period)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._h = None
+        with torch.cuda.device(self.device):
+            self._h = _lib.tt_channel_create(self.C, self.L, d.ctypes.data, self.S, int(seed), int(snapshot_capacity),
+                                             int(channel_offset))
+
+    # -- lifecycle -------------------------------------------------------------------
+    def close(self) -> None:
+        if self._h is not None:
+            _lib.tt_channel_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> int:
+        if self._h is None:
+            raise RuntimeError("channel is closed")
+        return self._h
+
+    def info(self) -> _lib.ChannelInfo:
+        return _lib.tt_channel_get_info(self.handle)
+
+    @property
+    def t(self) -> int:
+        return int(self.info().t)
+
+    # -- calls -----------------------------------------------------------------------
+    def load_snapshots(self, gains, first_index: int, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """gains: float32 [C][count][L][2] (torch tensor on this device or host, or numpy)."""
+        if isinstance(gains, np.ndarray):
+            g = np.ascontiguousarray(gains, dtype=np.float32)
+            ptr, count = g.ctypes.data, g.shape[1]
+            keep = g
+        else:
+            g = gains.contiguous()
+            if g.dtype != torch.float32:
+                raise TypeError("gains must be float32")
+            ptr, count = g.data_ptr(), g.shape[1]
+            keep = g
+        if tuple(keep.shape[:1]) != (self.C,) or keep.shape[2:] != (self.L, 2):
+            raise ValueError(f"gains must be [C={self.C}][count][L={self.L}][2], got {tuple(keep.shape)}")
+        _lib.tt_channel_load_snapshots(self.handle, ptr, int(first_index), int(count), _stream_ptr(stream))
+        if isinstance(keep, np.ndarray):
+            # host pageable source: make sure the copy has consumed it before returning
+            torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+
+    def apply(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, noise_sigma: float = 0.0,
+              stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """x: float32 device tensor [C][n][2] (or complex64 [C][n]); returns y alike."""
+        xv = torch.view_as_real(x) if x.is_complex() else x
+        if xv.dtype != torch.float32 or xv.dim() != 3 or xv.shape[0] != self.C or xv.shape[2] != 2:
+            raise ValueError(f"x must be float32 [C={self.C}][n][2] or complex64 [C][n]")
+        if not xv.is_contiguous():
+            raise ValueError("x must be contiguous")
+        if out is None:
+            out = torch.empty_like(x)
+        ov = torch.view_as_real(out) if out.is_complex() else out
+        if ov.shape != xv.shape or not ov.is_contiguous() or ov.dtype != torch.float32:
+            raise ValueError("out must match x")
+        _lib.tt_channel_apply(self.handle, xv.data_ptr(), ov.data_ptr(), int(xv.shape[1]), float(noise_sigma),
+                              _stream_ptr(stream))
+        return out
+
+    def apply_host(self, x: torch.Tensor, out: torch.Tensor, noise_sigma: float = 0.0,
+                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Host tensors (pinned for overlap) [C][n][2]; out is complete when `stream` gets here."""
+        if x.device.type != "cpu" or out.device.type != "cpu":
+            raise ValueError("apply_host takes host tensors")
+        if x.dtype != torch.float32 or x.dim() != 3 or x.shape[0] != self.C or x.shape[2] != 2 or \
+                out.shape != x.shape or not (x.is_contiguous() and out.is_contiguous()):
+            raise ValueError(f"x, out must be contiguous float32 [C={self.C}][n][2]")
+        _lib.tt_channel_apply_host(self.handle, x.data_ptr(), out.data_ptr(), int(x.shape[1]), float(noise_sigma),
+                                   _stream_ptr(stream))
+        return out
+
+    def reset(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        _lib.tt_channel_reset(self.handle, _stream_ptr(stream))

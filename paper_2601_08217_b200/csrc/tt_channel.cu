@@ -1,0 +1,485 @@
+// tt_channel.cu — host side of the C ABI in include/tt_channel.h: handle ownership,
+// validation, snapshot ring residency, the delay-line ping-pong, launch planning,
+// and the pipelined host-buffer path. Every arithmetic step of the channel runs in
+// the kernels of tt_conv.cuh; nothing here touches sample values.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "tt_channel.h"
+#include "tt_conv.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+tt_status fail(tt_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+tt_status cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear a sticky-free error so later calls are not poisoned
+    if (e == cudaErrorMemoryAllocation) return fail(TT_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    return fail(TT_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define TT_CUDA(call, what)                         \
+    do {                                            \
+        cudaError_t e__ = (call);                   \
+        if (e__ != cudaSuccess) return cuda_fail(e__, what); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess) ok = (prev == dev) || (cudaSetDevice(dev) == cudaSuccess);
+    }
+    ~DeviceGuard() {
+        if (ok && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Launch plan of the tiled kernel for one handle / call shape.
+struct Plan {
+    int R = 0;           // outputs per thread (0 = generic kernel)
+    size_t smem = 0;     // dynamic shared memory bytes
+    int nk_max = 0;
+};
+
+constexpr size_t kSmemBudget = 112 * 1024;  // two CTAs per SM (228 KB per SM)
+
+size_t smem_bytes(int R, int H, int L, int Lp, int S, int* nk_out) {
+    const int T = tt::kThreads * R;
+    const int nk = (T - 1) / S + 2;  // worst-case intervals touched by a tile
+    *nk_out = nk;
+    const size_t W = static_cast<size_t>(H) + T;
+    const size_t RAW = static_cast<size_t>(nk + 1) * Lp;
+    return 128 + 2 * W * 8 + 2 * RAW * 8 + static_cast<size_t>(nk) * L * 16 + static_cast<size_t>(L) * 4;
+}
+
+}  // namespace
+
+struct tt_channel_s {
+    int dev = 0;
+    int num_sms = 148;
+    int C = 0, L = 0, Lp = 0, S = 0, H = 0, maxD = 0;
+    uint64_t seed = 0;
+    int64_t cap = 0, chan_off = 0;
+    int64_t t = 0;
+    int p = 0;  // history buffer holding the current delay line
+    int64_t res_lo = 0, res_hi = 0;
+    float2* ring = nullptr;
+    float2* hist = nullptr;  // [2][C][H]
+    int32_t* dsort = nullptr;
+    int32_t* perm = nullptr;
+    size_t dev_bytes = 0;
+    Plan plan;
+    int occ[4] = {0, 0, 0, 0};  // resident CTAs per SM for R = 8, 4, 2, generic
+    // host-buffer path
+    float2* stage = nullptr;  // 3 x (in + out) chunk buffers
+    size_t stage_elems = 0;   // float2 per in (or out) chunk buffer
+    cudaStream_t cs_h2d = nullptr, cs_d2h = nullptr;
+    cudaEvent_t ev_h2d[3] = {}, ev_k[3] = {}, ev_free[3] = {}, ev_start = nullptr;
+};
+
+namespace {
+
+template <int R, bool NOISE>
+cudaError_t prepare_kernel(size_t smem, int* occ) {
+    auto k = tt::tt_conv_kernel<R, NOISE>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, tt::kThreads, smem);
+}
+
+cudaError_t prepare_plan(tt_channel_s* h) {
+    // largest R whose double-buffered plan fits two CTAs per SM; else the generic kernel
+    const int Rs[3] = {8, 4, 2};
+    h->plan = Plan{};
+    for (int i = 0; i < 3; ++i) {
+        int nk = 0;
+        const size_t sm = smem_bytes(Rs[i], h->H, h->L, h->Lp, h->S, &nk);
+        if (sm <= kSmemBudget) {
+            h->plan.R = Rs[i];
+            h->plan.smem = sm;
+            h->plan.nk_max = nk;
+            break;
+        }
+    }
+    if (h->plan.R == 0) return cudaSuccess;
+    int o0 = 0, o1 = 0;
+    cudaError_t e;
+    switch (h->plan.R) {
+        case 8:
+            if ((e = prepare_kernel<8, false>(h->plan.smem, &o0)) != cudaSuccess) return e;
+            if ((e = prepare_kernel<8, true>(h->plan.smem, &o1)) != cudaSuccess) return e;
+            break;
+        case 4:
+            if ((e = prepare_kernel<4, false>(h->plan.smem, &o0)) != cudaSuccess) return e;
+            if ((e = prepare_kernel<4, true>(h->plan.smem, &o1)) != cudaSuccess) return e;
+            break;
+        default:
+            if ((e = prepare_kernel<2, false>(h->plan.smem, &o0)) != cudaSuccess) return e;
+            if ((e = prepare_kernel<2, true>(h->plan.smem, &o1)) != cudaSuccess) return e;
+            break;
+    }
+    h->occ[0] = std::max(1, o0);
+    h->occ[1] = std::max(1, o1);
+    return cudaSuccess;
+}
+
+// Enqueue the convolution of channels [c_lo, c_hi) for this call (no state change).
+tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int32_t c_hi, int64_t n, float sigma,
+                 cudaStream_t st) {
+    tt::ConvParams p{};
+    p.x = x;
+    p.y = y;
+    const size_t hs = static_cast<size_t>(h->C) * h->H;
+    p.hist_rd = h->hist + h->p * hs;
+    p.hist_wr = h->hist + (1 - h->p) * hs;
+    p.ring = h->ring;
+    p.dsort = h->dsort;
+    p.perm = h->perm;
+    p.n = n;
+    p.t = h->t;
+    p.cap = h->cap;
+    p.chan_offset = h->chan_off;
+    p.c_lo = c_lo;
+    p.L = h->L;
+    p.Lp = h->Lp;
+    p.H = h->H;
+    p.S = h->S;
+    p.key0 = static_cast<uint32_t>(h->seed);
+    p.key1 = static_cast<uint32_t>(h->seed >> 32);
+    // docs/tt-normal-v1.md §3: sigma / sqrt(2) rounded once in double, then to float
+    p.noise_sc = static_cast<float>(static_cast<double>(sigma) * 0x1.6a09e667f3bcdp-1);
+    const bool noise = sigma > 0.0f;
+    const int nch = c_hi - c_lo;
+    if (h->plan.R != 0) {
+        const int T = tt::kThreads * h->plan.R;
+        p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
+        p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
+        p.nk_max = h->plan.nk_max;
+        const int occ = noise ? h->occ[1] : h->occ[0];
+        const int64_t grid = std::min<int64_t>(p.total_tiles, static_cast<int64_t>(h->num_sms) * occ);
+        const dim3 g(static_cast<unsigned>(grid)), b(tt::kThreads);
+        const size_t sm = h->plan.smem;
+        switch (h->plan.R * 2 + (noise ? 1 : 0)) {
+            case 16: tt::tt_conv_kernel<8, false><<<g, b, sm, st>>>(p); break;
+            case 17: tt::tt_conv_kernel<8, true><<<g, b, sm, st>>>(p); break;
+            case 8: tt::tt_conv_kernel<4, false><<<g, b, sm, st>>>(p); break;
+            case 9: tt::tt_conv_kernel<4, true><<<g, b, sm, st>>>(p); break;
+            case 4: tt::tt_conv_kernel<2, false><<<g, b, sm, st>>>(p); break;
+            default: tt::tt_conv_kernel<2, true><<<g, b, sm, st>>>(p); break;
+        }
+    } else {
+        p.tiles_per_ch = 1;
+        p.total_tiles = nch;
+        const int64_t N = static_cast<int64_t>(nch) * n;
+        const int64_t grid = std::min<int64_t>((N + tt::kThreads - 1) / tt::kThreads, int64_t(h->num_sms) * 8);
+        if (noise)
+            tt::tt_conv_generic_kernel<true><<<static_cast<unsigned>(grid), tt::kThreads, 0, st>>>(p);
+        else
+            tt::tt_conv_generic_kernel<false><<<static_cast<unsigned>(grid), tt::kThreads, 0, st>>>(p);
+        if (h->H > 0) {
+            const int64_t tot = static_cast<int64_t>(nch) * h->H;
+            const int64_t hg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);
+            tt::tt_history_kernel<<<static_cast<unsigned>(hg), 256, 0, st>>>(p, nch);
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    return TT_OK;
+}
+
+tt_status check_apply(tt_channel_s* h, const void* in, const void* out, int64_t n, float sigma) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    if (!in || !out) return fail(TT_ERR_INVALID_ARG, "NULL in/out");
+    if (n <= 0) return fail(TT_ERR_INVALID_ARG, "n_samples must be > 0 (got %lld)", (long long)n);
+    if (in == out) return fail(TT_ERR_INVALID_ARG, "in and out must not overlap");
+    if (!(sigma >= 0.0f) || !std::isfinite(sigma)) return fail(TT_ERR_INVALID_ARG, "noise_sigma must be finite and >= 0");
+    const int64_t k_lo = h->t / h->S;
+    const int64_t k_hi = (h->t + n - 1) / h->S + 1;
+    if (h->res_hi <= h->res_lo || k_lo < h->res_lo || k_hi >= h->res_hi)
+        return fail(TT_ERR_SNAPSHOT_MISSING, "apply needs snapshots [%lld, %lld] but [%lld, %lld) are resident",
+                    (long long)k_lo, (long long)k_hi, (long long)h->res_lo, (long long)h->res_hi);
+    return TT_OK;
+}
+
+void free_all(tt_channel_s* h) {
+    cudaFree(h->ring);
+    cudaFree(h->hist);
+    cudaFree(h->dsort);
+    cudaFree(h->perm);
+    cudaFree(h->stage);
+    for (int i = 0; i < 3; ++i) {
+        if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
+        if (h->ev_k[i]) cudaEventDestroy(h->ev_k[i]);
+        if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
+    }
+    if (h->ev_start) cudaEventDestroy(h->ev_start);
+    if (h->cs_h2d) cudaStreamDestroy(h->cs_h2d);
+    if (h->cs_d2h) cudaStreamDestroy(h->cs_d2h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t tt_abi_version(void) { return TT_ABI_VERSION; }
+
+const char* tt_last_error(void) { return g_err; }
+
+const char* tt_status_string(tt_status s) {
+    switch (s) {
+        case TT_OK: return "TT_OK";
+        case TT_ERR_INVALID_ARG: return "TT_ERR_INVALID_ARG";
+        case TT_ERR_OUT_OF_MEMORY: return "TT_ERR_OUT_OF_MEMORY";
+        case TT_ERR_CUDA: return "TT_ERR_CUDA";
+        case TT_ERR_SNAPSHOT_MISSING: return "TT_ERR_SNAPSHOT_MISSING";
+        case TT_ERR_UNSUPPORTED: return "TT_ERR_UNSUPPORTED";
+    }
+    return "TT_ERR_UNKNOWN";
+}
+
+tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps, const int32_t* delays,
+                            int32_t snapshot_period, uint64_t seed, int64_t snapshot_capacity,
+                            int64_t channel_offset) {
+    if (!out) return fail(TT_ERR_INVALID_ARG, "NULL out");
+    *out = nullptr;
+    if (num_ue <= 0) return fail(TT_ERR_INVALID_ARG, "num_ue must be > 0");
+    if (num_taps <= 0 || num_taps > TT_MAX_TAPS) return fail(TT_ERR_INVALID_ARG, "num_taps must be in [1, %d]", TT_MAX_TAPS);
+    if (!delays) return fail(TT_ERR_INVALID_ARG, "NULL delays");
+    if (snapshot_period <= 0) return fail(TT_ERR_INVALID_ARG, "snapshot_period must be > 0");
+    if (snapshot_capacity < 2) return fail(TT_ERR_INVALID_ARG, "snapshot_capacity must be >= 2");
+    if (channel_offset < 0) return fail(TT_ERR_INVALID_ARG, "channel_offset must be >= 0");
+    const int64_t CL = static_cast<int64_t>(num_ue) * num_taps;
+    int maxD = 0;
+    for (int64_t i = 0; i < CL; ++i) {
+        if (delays[i] < 0 || delays[i] > TT_MAX_DELAY)
+            return fail(TT_ERR_INVALID_ARG, "delay[%lld] = %d outside [0, %d]", (long long)i, delays[i], TT_MAX_DELAY);
+        maxD = std::max(maxD, static_cast<int>(delays[i]));
+    }
+    int dev = 0;
+    TT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    cudaDeviceProp prop;
+    TT_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    if (prop.major != 10) return fail(TT_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a", dev, prop.major, prop.minor);
+
+    tt_channel_s* h = new (std::nothrow) tt_channel_s();
+    if (!h) return fail(TT_ERR_OUT_OF_MEMORY, "host allocation");
+    h->dev = dev;
+    h->num_sms = prop.multiProcessorCount;
+    h->C = num_ue;
+    h->L = num_taps;
+    h->Lp = (num_taps + 1) & ~1;
+    h->S = snapshot_period;
+    h->maxD = maxD;
+    h->H = (maxD + 1) & ~1;
+    h->seed = seed;
+    h->cap = snapshot_capacity;
+    h->chan_off = channel_offset;
+
+    // sorted-by-delay tap order per channel (stable: ties keep tap index order)
+    std::vector<int32_t> ds(CL), pm(CL);
+    for (int c = 0; c < num_ue; ++c) {
+        int32_t* pc = pm.data() + static_cast<int64_t>(c) * num_taps;
+        std::iota(pc, pc + num_taps, 0);
+        const int32_t* dc = delays + static_cast<int64_t>(c) * num_taps;
+        std::stable_sort(pc, pc + num_taps, [dc](int32_t a, int32_t b) { return dc[a] < dc[b]; });
+        for (int j = 0; j < num_taps; ++j) ds[static_cast<int64_t>(c) * num_taps + j] = dc[pc[j]];
+    }
+    auto bail = [&](tt_status s) {
+        free_all(h);
+        delete h;
+        return s;
+    };
+    cudaError_t e;
+    const size_t ring_b = static_cast<size_t>(num_ue) * snapshot_capacity * h->Lp * sizeof(float2);
+    const size_t hist_b = 2 * static_cast<size_t>(num_ue) * h->H * sizeof(float2);
+    const size_t tab_b = static_cast<size_t>(CL) * sizeof(int32_t);
+    if ((e = cudaMalloc(&h->ring, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(snapshot ring)"));
+    if (hist_b && (e = cudaMalloc(&h->hist, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(history)"));
+    if ((e = cudaMalloc(&h->dsort, tab_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(delays)"));
+    if ((e = cudaMalloc(&h->perm, tab_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
+    h->dev_bytes = ring_b + hist_b + 2 * tab_b;
+    if ((e = cudaMemcpy(h->dsort, ds.data(), tab_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy delays"));
+    if ((e = cudaMemcpy(h->perm, pm.data(), tab_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
+    if (hist_b && (e = cudaMemset(h->hist, 0, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "zero history"));
+    // the ring is zeroed so a never-loaded slot can never inject NaN into a CTA's
+    // table (apply refuses non-resident ranges anyway)
+    if ((e = cudaMemset(h->ring, 0, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "zero ring"));
+    if ((e = prepare_plan(h)) != cudaSuccess) return bail(cuda_fail(e, "kernel setup"));
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(cuda_fail(e, "create sync"));
+    *out = h;
+    return TT_OK;
+}
+
+tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t first_index, int64_t count,
+                                    tt_stream_t stream) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    if (!gains) return fail(TT_ERR_INVALID_ARG, "NULL gains");
+    if (first_index < 0 || count <= 0) return fail(TT_ERR_INVALID_ARG, "need first_index >= 0 and count > 0");
+    if (count > h->cap) return fail(TT_ERR_INVALID_ARG, "count %lld exceeds snapshot_capacity %lld", (long long)count, (long long)h->cap);
+    DeviceGuard dg(h->dev);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // [C][count][L] float2 (pitch L) -> ring [C][cap][Lp] at slots (first + i) mod cap:
+    // one 3-D pitched copy per contiguous slot range (at most two)
+    int64_t done = 0;
+    while (done < count) {
+        const int64_t k = first_index + done;
+        const int64_t slot = k % h->cap;
+        const int64_t m = std::min(count - done, h->cap - slot);
+        cudaMemcpy3DParms cp{};
+        cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(gains), static_cast<size_t>(h->L) * sizeof(float2),
+                                        static_cast<size_t>(h->L), static_cast<size_t>(count));
+        cp.srcPos = make_cudaPos(0, static_cast<size_t>(done), 0);
+        cp.dstPtr = make_cudaPitchedPtr(h->ring, static_cast<size_t>(h->Lp) * sizeof(float2), static_cast<size_t>(h->Lp),
+                                        static_cast<size_t>(h->cap));
+        cp.dstPos = make_cudaPos(0, static_cast<size_t>(slot), 0);
+        cp.extent = make_cudaExtent(static_cast<size_t>(h->L) * sizeof(float2), static_cast<size_t>(m),
+                                    static_cast<size_t>(h->C));
+        cp.kind = cudaMemcpyDefault;
+        TT_CUDA(cudaMemcpy3DAsync(&cp, st), "snapshot copy");
+        done += m;
+    }
+    const int64_t lo = first_index, hi = first_index + count;
+    if (h->res_hi > h->res_lo && lo >= h->res_lo && lo <= h->res_hi) {
+        h->res_hi = std::max(h->res_hi, hi);
+        h->res_lo = std::max(h->res_lo, h->res_hi - h->cap);
+    } else {
+        h->res_lo = lo;
+        h->res_hi = hi;
+    }
+    return TT_OK;
+}
+
+tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
+                           tt_stream_t stream) {
+    tt_status s = check_apply(h, in, out, n_samples, noise_sigma);
+    if (s != TT_OK) return s;
+    DeviceGuard dg(h->dev);
+    s = launch(h, reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), 0, h->C, n_samples,
+               noise_sigma, static_cast<cudaStream_t>(stream));
+    if (s != TT_OK) return s;
+    h->t += n_samples;
+    if (h->H > 0) h->p ^= 1;
+    return TT_OK;
+}
+
+tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
+                                tt_stream_t stream) {
+    tt_status s = check_apply(h, in, out, n_samples, noise_sigma);
+    if (s != TT_OK) return s;
+    DeviceGuard dg(h->dev);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // chunk of channels per pipeline stage: ~64 MiB of input, at least one channel
+    const int64_t per_ch = n_samples;
+    int64_t cc = std::max<int64_t>(1, (int64_t(64) << 20) / (per_ch * 8));
+    cc = std::min<int64_t>(cc, h->C);
+    const size_t need = static_cast<size_t>(cc * per_ch);
+    if (need > h->stage_elems) {
+        if (h->stage) {
+            TT_CUDA(cudaStreamSynchronize(h->cs_d2h), "staging drain");
+            cudaFree(h->stage);
+            h->stage = nullptr;
+            h->stage_elems = 0;
+        }
+        TT_CUDA(cudaMalloc(&h->stage, need * 6 * sizeof(float2)), "cudaMalloc(host-path staging)");
+        h->stage_elems = need;
+        if (!h->cs_h2d) {
+            TT_CUDA(cudaStreamCreateWithFlags(&h->cs_h2d, cudaStreamNonBlocking), "stream create");
+            TT_CUDA(cudaStreamCreateWithFlags(&h->cs_d2h, cudaStreamNonBlocking), "stream create");
+            for (int i = 0; i < 3; ++i) {
+                TT_CUDA(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming), "event create");
+                TT_CUDA(cudaEventCreateWithFlags(&h->ev_k[i], cudaEventDisableTiming), "event create");
+                TT_CUDA(cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming), "event create");
+                TT_CUDA(cudaEventRecord(h->ev_free[i], h->cs_d2h), "event record");
+            }
+            TT_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event create");
+        }
+    }
+    // the copy streams start after everything already enqueued on `stream`
+    TT_CUDA(cudaEventRecord(h->ev_start, st), "event record");
+    TT_CUDA(cudaStreamWaitEvent(h->cs_h2d, h->ev_start, 0), "stream wait");
+    const float2* hin = reinterpret_cast<const float2*>(in);
+    float2* hout = reinterpret_cast<float2*>(out);
+    int i = 0;
+    for (int64_t c0 = 0; c0 < h->C; c0 += cc, ++i) {
+        const int b = i % 3;
+        const int64_t c1 = std::min<int64_t>(h->C, c0 + cc);
+        const size_t bytes = static_cast<size_t>((c1 - c0) * per_ch) * sizeof(float2);
+        float2* din = h->stage + static_cast<size_t>(b) * 2 * need;
+        float2* dout = din + need;
+        TT_CUDA(cudaStreamWaitEvent(h->cs_h2d, h->ev_free[b], 0), "stream wait");
+        TT_CUDA(cudaMemcpyAsync(din, hin + c0 * per_ch, bytes, cudaMemcpyHostToDevice, h->cs_h2d), "H2D");
+        TT_CUDA(cudaEventRecord(h->ev_h2d[b], h->cs_h2d), "event record");
+        TT_CUDA(cudaStreamWaitEvent(st, h->ev_h2d[b], 0), "stream wait");
+        s = launch(h, din, dout, static_cast<int32_t>(c0), static_cast<int32_t>(c1), n_samples, noise_sigma, st);
+        if (s != TT_OK) return s;
+        TT_CUDA(cudaEventRecord(h->ev_k[b], st), "event record");
+        TT_CUDA(cudaStreamWaitEvent(h->cs_d2h, h->ev_k[b], 0), "stream wait");
+        TT_CUDA(cudaMemcpyAsync(hout + c0 * per_ch, dout, bytes, cudaMemcpyDeviceToHost, h->cs_d2h), "D2H");
+        TT_CUDA(cudaEventRecord(h->ev_free[b], h->cs_d2h), "event record");
+    }
+    // `stream` reaches this point only when every D2H has landed
+    TT_CUDA(cudaEventRecord(h->ev_start, h->cs_d2h), "event record");
+    TT_CUDA(cudaStreamWaitEvent(st, h->ev_start, 0), "stream wait");
+    h->t += n_samples;
+    if (h->H > 0) h->p ^= 1;
+    return TT_OK;
+}
+
+tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    DeviceGuard dg(h->dev);
+    if (h->hist)
+        TT_CUDA(cudaMemsetAsync(h->hist, 0, 2 * static_cast<size_t>(h->C) * h->H * sizeof(float2),
+                                static_cast<cudaStream_t>(stream)),
+                "zero history");
+    h->t = 0;
+    h->p = 0;
+    return TT_OK;
+}
+
+tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
+    if (!h || !info) return fail(TT_ERR_INVALID_ARG, "NULL handle or info");
+    info->num_ue = h->C;
+    info->num_taps = h->L;
+    info->snapshot_period = h->S;
+    info->history = h->H;
+    info->max_delay = h->maxD;
+    info->device = h->dev;
+    info->t = h->t;
+    info->snapshot_capacity = h->cap;
+    info->resident_lo = h->res_lo;
+    info->resident_hi = h->res_hi;
+    info->channel_offset = h->chan_off;
+    info->seed = h->seed;
+    info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2));
+    info->outputs_per_thread = h->plan.R;
+    info->launches_per_apply = h->plan.R != 0 ? 1 : (h->H > 0 ? 2 : 1);
+    return TT_OK;
+}
+
+tt_status tt_channel_destroy(tt_channel_t h) {
+    if (!h) return TT_OK;
+    DeviceGuard dg(h->dev);
+    cudaDeviceSynchronize();
+    free_all(h);
+    delete h;
+    return TT_OK;
+}
+
+}  // extern "C"

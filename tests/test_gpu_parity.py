@@ -1,0 +1,161 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle on the same seeded
+inputs: every BASELINE config (scaled to oracle-friendly sizes that still span many
+tiles and a ragged tail), closed-form special cases bit-exactly, streaming /
+isolation / sharding invariances, the bit-exact noise, the generic kernel, the
+host-buffer path, and error codes."""
+import numpy as np
+import pytest
+
+import oracle
+import ttsynth
+from harness import Run, compare, to_c
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("c1", {}),                                                        # full size
+    ("c2", dict(n_per_call=300_001)),                                  # ragged tail, noise
+    ("c3", dict(ues=4, calls=3)),                                      # streaming slots, DL+UL
+    ("c4", dict(ues=3, calls=3)),
+    ("c5-L1", dict(ues=4, n_per_call=100_003)),
+    ("c5-L4", dict(ues=4, n_per_call=100_003)),
+    ("c5-L16", dict(ues=4, n_per_call=100_003)),
+    ("c5-L64", dict(ues=2, n_per_call=65_537)),
+    ("c5-L256", dict(ues=2, n_per_call=40_001)),
+])
+def test_config_parity(cuda_device, name, kw):
+    w = ttsynth.get(name).scaled(**kw)
+    run = Run(w, seed=1234)
+    y = run.gpu(cuda_device)
+    compare(y, run.oracle(), name)
+
+
+def test_identity_bit_exact(cuda_device):
+    """L=1, d=0, g == 1 -> y == x bit for bit (fma(a, 0, 1) = 1; the cross term is 0)."""
+    w = ttsynth.get("c1").scaled(fixed_delays=(0,), fixed_pdp=(1.0,), L=1, D=0, S=64, n_per_call=10_001)
+    run = Run(w)
+    run.gains[...] = 0.0
+    run.gains[..., 0] = 1.0
+    y = run.gpu(cuda_device)
+    assert np.array_equal(y, run.x)
+
+
+def test_pure_delay_bit_exact(cuda_device):
+    D = 777
+    w = ttsynth.get("c1").scaled(fixed_delays=(D,), fixed_pdp=(1.0,), L=1, D=D, S=100, n_per_call=5_000, calls=3)
+    run = Run(w)
+    run.gains[...] = 0.0
+    run.gains[..., 0] = 1.0
+    y = run.gpu(cuda_device, calls=[100, 4_000, 10_900])
+    assert np.all(y[:, :D] == 0)
+    assert np.array_equal(y[:, D:], run.x[:, :-D])
+
+
+def test_streaming_bit_identical_any_partition(cuda_device):
+    """slot-streamed output with carried history == one-shot, here bit for bit,
+    for partitions with n < H, odd n, and n not a multiple of anything."""
+    w = ttsynth.get("c4").scaled(ues=2, n_per_call=20_000, calls=1)
+    run = Run(w, seed=5)
+    one = run.gpu(cuda_device, calls=[20_000])
+    for calls in ([1, 2, 3, 1000, 1023, 17_971], [999, 5, 19_996], [7_001, 7_001, 5_998], [4_096] * 4 + [3_616]):
+        y = run.gpu(cuda_device, calls=calls)
+        assert np.array_equal(y, one), calls
+    compare(one, run.oracle(), "c4 scaled")
+
+
+def test_isolation(cuda_device):
+    """S:357 / P:23 per-UE isolation: changing channel 1's taps leaves channel 0 and 2
+    bit-identical."""
+    w = ttsynth.get("c3").scaled(ues=2, dirs=1, n_per_call=9_000, calls=2)
+    a = Run(w, seed=3)
+    b = Run(w, seed=3)
+    b.gains[1] *= -0.5
+    b.gains[1, :, 0] += 0.25
+    ya, yb = a.gpu(cuda_device), b.gpu(cuda_device)
+    assert np.array_equal(ya[0], yb[0])
+    assert not np.array_equal(ya[1], yb[1])
+
+
+def test_sharding_invariance(cuda_device):
+    """Two handles over channel blocks with global channel offsets == one handle."""
+    w = ttsynth.get("c3").scaled(ues=6, n_per_call=5_000, calls=2)
+    full = Run(w, seed=11).gpu(cuda_device)
+    for lo, hi in ((0, 4), (4, 10), (10, 12)):
+        part = Run(w, lo, hi, seed=11).gpu(cuda_device)
+        assert np.array_equal(part, full[lo:hi]), (lo, hi)
+
+
+def test_noise_bit_exact(cuda_device):
+    """x == 0 -> y == w; GPU noise equals the oracle's bit for bit, for even and odd
+    call starts (both Philox sharing paths)."""
+    w = ttsynth.get("c2").scaled(ues=3, n_per_call=12_345, calls=1)
+    run = Run(w, seed=0xDEADBEEF12345)
+    run.x[...] = 0.0
+    y = run.gpu(cuda_device, calls=[1, 6_000, 6_344])
+    for c in range(run.C):
+        ref = oracle.noise_block(run.seed, c, 0, run.N, run.sigma)
+        assert np.array_equal(y[c], ref), c
+
+
+def test_generic_kernel_path(cuda_device):
+    """A plan that does not fit shared memory (long filter, S = 1) takes the generic
+    kernel; it matches the oracle and the streaming invariance still holds."""
+    rng = np.random.default_rng(0)
+    L = 1500
+    w = ttsynth.get("c2").scaled(ues=2, L=L, D=3000, S=1, n_per_call=3_001, snr_db=10.0)
+    run = Run(w, seed=2)
+    y1 = run.gpu(cuda_device)
+    y2 = run.gpu(cuda_device, calls=[1_000, 2_001])
+    assert np.array_equal(y1, y2)
+    compare(y1, run.oracle(), "generic")
+
+
+def test_host_buffer_path_equals_device_path(cuda_device):
+    w = ttsynth.get("c3").scaled(ues=5, n_per_call=7_000, calls=2)
+    run = Run(w, seed=4)
+    assert np.array_equal(run.gpu(cuda_device, host_path=True), run.gpu(cuda_device))
+
+
+def test_snapshot_ring_streaming(cuda_device):
+    """A ring smaller than the run, refilled slot by slot (as a streaming user would)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    w = ttsynth.get("c4").scaled(ues=2, calls=4)
+    run = Run(w, seed=8)
+    ref = run.gpu(cuda_device)
+    per = w.n_per_call // w.S
+    ch = Channel(run.delays, w.S, seed=8, snapshot_capacity=per + 2, device=cuda_device)
+    g = torch.from_numpy(run.gains).to(cuda_device)
+    out = []
+    for s in range(w.calls):
+        lo = s * per
+        hi = min(run.K, (s + 1) * per + 2)
+        ch.load_snapshots(g[:, lo:hi].contiguous(), lo)
+        xs = torch.from_numpy(np.ascontiguousarray(run.x[:, s * w.n_per_call:(s + 1) * w.n_per_call])).to(cuda_device)
+        out.append(ch.apply(xs, noise_sigma=run.sigma).cpu().numpy())
+    ch.close()
+    assert np.array_equal(np.concatenate(out, axis=1), ref)
+
+
+def test_error_codes(cuda_device):
+    import torch
+
+    from paper_2601_08217_b200 import Channel, TTError
+
+    ch = Channel([[0, 3]], 16, snapshot_capacity=4, device=cuda_device)
+    x = torch.zeros((1, 64, 2), device=cuda_device)
+    with pytest.raises(TTError, match="SNAPSHOT_MISSING"):
+        ch.apply(x)
+    ch.load_snapshots(torch.zeros((1, 4, 2, 2), device=cuda_device), 0)  # k = 0..3 -> n < 48
+    ch.apply(x[:, :47])
+    with pytest.raises(TTError, match="SNAPSHOT_MISSING"):
+        ch.apply(x[:, :2])  # needs k = 3 and 4
+    with pytest.raises(TTError, match="INVALID_ARG"):
+        ch.apply(x, out=x)
+    with pytest.raises(TTError, match="INVALID_ARG"):
+        ch.apply(x[:, :1], noise_sigma=-1.0)
+    assert ch.t == 47  # failed calls do not advance the stream
+    ch.close()

@@ -251,7 +251,7 @@ def main():
     # ---- this rank's shard (contiguous UE block; DL/UL of a UE stay together) ----------
     c_lo, c_hi = ttsynth.shard_ues(w, rank, world)
     C, n = c_hi - c_lo, w.n_per_call
-    steps_total = args.warmup + args.steps
+    steps_total = args.warmup + args.steps + max(args.e2e_steps, 0) + 1
     K = (steps_total * n - 1) // w.S + 2
     delays = ttsynth.delays(w, c_lo, c_hi)
     gains = ttsynth.snapshots(w, c_lo, c_hi, K, backend="torch", device=dev)

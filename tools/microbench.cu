@@ -93,6 +93,80 @@ __global__ void k_mac_reg(float* out, long long* cyc, float4 q) {
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// MAC-body variants (operands in registers). MODE 0: per output h/A/B FFMA2 (kernel v1);
+// 1: all h first (FFMA2) then A/B FFMA2; 2: all h first (scalar) then 4 scalar FFMA in
+// reuse-friendly order; 3: scalar with 2 chained accumulators; 4: h FFMA2 first, MAC scalar.
+template <int MODE>
+__global__ void k_mac_var(float* out, long long* cyc, float4 q, const float* init) {
+    float2 A[8], B[8], x[8];
+    float al[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        A[r] = B[r] = make_float2(0, 0);
+        x[r] = make_float2(init[threadIdx.x + r], init[threadIdx.x + r + 8]);
+        al[r] = init[threadIdx.x + r + 16];
+    }
+    __syncthreads();
+    long long t0 = clock64();
+    for (int it = 0; it < ITERS / 4; ++it) {
+        const float2 g = make_float2(q.x + it, q.y - it), dg = make_float2(q.z, q.w);
+        if (MODE == 0) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const float2 h = __ffma2_rn(make_float2(al[r], al[r]), dg, g);
+                A[r] = __ffma2_rn(make_float2(h.x, h.x), x[r], A[r]);
+                B[r] = __ffma2_rn(make_float2(h.y, h.y), x[r], B[r]);
+            }
+        } else if (MODE == 1 || MODE == 4) {
+            float2 h[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) h[r] = __ffma2_rn(make_float2(al[r], al[r]), dg, g);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if (MODE == 1) {
+                    A[r] = __ffma2_rn(make_float2(h[r].x, h[r].x), x[r], A[r]);
+                    B[r] = __ffma2_rn(make_float2(h[r].y, h[r].y), x[r], B[r]);
+                } else {
+                    A[r].x = __fmaf_rn(h[r].x, x[r].x, A[r].x);
+                    B[r].x = __fmaf_rn(h[r].y, x[r].x, B[r].x);
+                    B[r].y = __fmaf_rn(h[r].y, x[r].y, B[r].y);
+                    A[r].y = __fmaf_rn(h[r].x, x[r].y, A[r].y);
+                }
+            }
+        } else if (MODE == 2) {
+            float hr[8], hi[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) hr[r] = __fmaf_rn(al[r], dg.x, g.x);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) hi[r] = __fmaf_rn(al[r], dg.y, g.y);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                A[r].x = __fmaf_rn(hr[r], x[r].x, A[r].x);
+                B[r].x = __fmaf_rn(hi[r], x[r].x, B[r].x);
+                B[r].y = __fmaf_rn(hi[r], x[r].y, B[r].y);
+                A[r].y = __fmaf_rn(hr[r], x[r].y, A[r].y);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const float hr = __fmaf_rn(al[r], dg.x, g.x), hi = __fmaf_rn(al[r], dg.y, g.y);
+                A[r].x = __fmaf_rn(hr, x[r].x, A[r].x);
+                A[r].x = __fmaf_rn(-hi, x[r].y, A[r].x);
+                A[r].y = __fmaf_rn(hr, x[r].y, A[r].y);
+                A[r].y = __fmaf_rn(hi, x[r].x, A[r].y);
+            }
+        }
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) s += A[r].x + A[r].y + B[r].x + B[r].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 // the kernel's real inner loop: x from shared memory (lane-interleaved, conflict-free)
 __global__ void k_mac_smem(float* out, long long* cyc, const int* dl, int L) {
     __shared__ float2 xs[2048 + 2048];
@@ -188,7 +262,14 @@ int main() {
     CK(cudaMalloc(&dl, 64 * sizeof(int)));
     CK(cudaMemcpy(dl, hd.data(), 64 * sizeof(int), cudaMemcpyHostToDevice));
     std::vector<long long> h(maxb);
-    for (int per_sm : {1, 2, 4, 8}) {
+    float* initp;
+    {
+        std::vector<float> hi(1024);
+        for (int i = 0; i < 1024; ++i) hi[i] = 0.001f * (i % 97) - 0.03f;
+        CK(cudaMalloc(&initp, 1024 * sizeof(float)));
+        CK(cudaMemcpy(initp, hi.data(), 1024 * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    for (int per_sm : {1, 2, 3}) {
         const int blocks = sms * per_sm;
         // warm-up + measure each kernel
         auto run = [&](const char* name, double ops_per_thread, auto launch) -> int {
@@ -206,6 +287,11 @@ int main() {
         run("ffma2_lanes_per_clk", 16.0 * ITERS, [&](int b) { k_ffma2<<<b, threads>>>(out, cyc, 0.999f, 1e-3f); });
         run("mac_reg_outtaps_per_clk", 8.0 * (ITERS / 4),
             [&](int b) { k_mac_reg<<<b, threads>>>(out, cyc, make_float4(1, 2, 3, 4)); });
+        run("mac_v0_outtaps_per_clk", 8.0 * (ITERS / 4), [&](int b) { k_mac_var<0><<<b, threads>>>(out, cyc, make_float4(1, 2, 3, 4), initp); });
+        run("mac_v1_outtaps_per_clk", 8.0 * (ITERS / 4), [&](int b) { k_mac_var<1><<<b, threads>>>(out, cyc, make_float4(1, 2, 3, 4), initp); });
+        run("mac_v2_outtaps_per_clk", 8.0 * (ITERS / 4), [&](int b) { k_mac_var<2><<<b, threads>>>(out, cyc, make_float4(1, 2, 3, 4), initp); });
+        run("mac_v3_outtaps_per_clk", 8.0 * (ITERS / 4), [&](int b) { k_mac_var<3><<<b, threads>>>(out, cyc, make_float4(1, 2, 3, 4), initp); });
+        run("mac_v4_outtaps_per_clk", 8.0 * (ITERS / 4), [&](int b) { k_mac_var<4><<<b, threads>>>(out, cyc, make_float4(1, 2, 3, 4), initp); });
         run("mac_smem_L48_outtaps_per_clk", 8.0 * 16 * 48, [&](int b) { k_mac_smem<<<b, threads>>>(out, cyc, dl, 48); });
         run("lds64_bytes_per_clk", 8.0 * 8 * (ITERS / 8), [&](int b) { k_lds64<<<b, threads>>>(out, cyc); });
     }

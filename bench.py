@@ -224,6 +224,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sigma", type=float, default=None, help="override the config's noise sigma (experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -265,7 +266,7 @@ def main():
     del gains
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    sigma = w.sigma
+    sigma = w.sigma if args.sigma is None else args.sigma
 
     # ---- device-resident timed region ----------------------------------------------
     for i in range(args.warmup):

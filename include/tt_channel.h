@@ -90,7 +90,8 @@ typedef struct {
  *   snapshot_capacity: snapshot slots per channel kept on the device (>= 2); a ring.
  *   channel_offset: global id of this handle's channel 0 (so a sharded run keys
  *     noise by global channel, NS "keyed by (seed, UE, sample)").
- * Binds to the current CUDA device. Allocates: the ring C x capacity x L x 8 B, the
+ * Binds to the current CUDA device. Allocates: the ring C x capacity x L x 16 B (each
+ * slot holds (g_k, g_{k+1} - g_k) per tap, taps sorted by delay), the
  * delay-line history 2 x C x H x 8 B, and small per-channel tables; zeroes the
  * history (R4) and sets t = 0.
  * Errors: INVALID_ARG (out == NULL, C <= 0, L <= 0 or > TT_MAX_TAPS, delays == NULL,

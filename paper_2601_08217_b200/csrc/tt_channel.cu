@@ -50,22 +50,23 @@ struct DeviceGuard {
     }
 };
 
-// Launch plan of the tiled kernel for one handle / call shape.
+// Launch plan of the tiled kernel for one handle.
 struct Plan {
-    int R = 0;           // outputs per thread (0 = generic kernel)
+    int R = 0;           // outputs per consumer thread (0 = generic kernel)
+    int stages = 0;      // shared-memory pipeline depth
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;
 };
 
-constexpr size_t kSmemBudget = 112 * 1024;  // two CTAs per SM (228 KB per SM)
+constexpr size_t kSmemBudget = 220 * 1024;  // one CTA per SM (227 KB max per CTA)
 
-size_t smem_bytes(int R, int H, int L, int Lp, int S, int* nk_out) {
-    const int T = tt::kThreads * R;
+// must match tt_conv_kernel's layout: 128 B of barriers + `stages` x [win | coef | xo]
+size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, int* nk_out) {
+    const int T = tt::kConsumerWarps * 32 * R;
     const int nk = (T - 1) / S + 2;  // worst-case intervals touched by a tile
     *nk_out = nk;
-    const size_t W = static_cast<size_t>(H) + T;
-    const size_t RAW = static_cast<size_t>(nk + 1) * Lp;
-    return 128 + 2 * W * 8 + 2 * RAW * 8 + static_cast<size_t>(nk) * L * 16 + static_cast<size_t>(L) * 4;
+    const size_t st = (static_cast<size_t>(H) + T) * 8 + static_cast<size_t>(nk) * L * 16 + static_cast<size_t>(L4) * 4;
+    return 128 + static_cast<size_t>(stages) * st;
 }
 
 }  // namespace
@@ -73,19 +74,21 @@ size_t smem_bytes(int R, int H, int L, int Lp, int S, int* nk_out) {
 struct tt_channel_s {
     int dev = 0;
     int num_sms = 148;
-    int C = 0, L = 0, Lp = 0, S = 0, H = 0, maxD = 0;
+    int C = 0, L = 0, L4 = 0, S = 0, H = 0, maxD = 0;
     uint64_t seed = 0;
     int64_t cap = 0, chan_off = 0;
     int64_t t = 0;
     int p = 0;  // history buffer holding the current delay line
     int64_t res_lo = 0, res_hi = 0;
-    float2* ring = nullptr;
-    float2* hist = nullptr;  // [2][C][H]
-    int32_t* dsort = nullptr;
-    int32_t* perm = nullptr;
+    float4* ring = nullptr;    // [C][cap][L] (g_k, g_{k+1} - g_k), taps sorted by delay
+    float2* hist = nullptr;    // [2][C][H] delay-line ping-pong
+    int32_t* perm = nullptr;   // [C][L] original tap index of sorted tap j
+    int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
+    float2* load_stage = nullptr;  // device staging for host-memory snapshot sources
+    size_t load_stage_elems = 0;
     size_t dev_bytes = 0;
     Plan plan;
-    int occ[4] = {0, 0, 0, 0};  // resident CTAs per SM for R = 8, 4, 2, generic
+    int occ[2] = {0, 0};  // resident CTAs per SM (no noise, noise)
     // host-buffer path
     float2* stage = nullptr;  // 3 x (in + out) chunk buffers
     size_t stage_elems = 0;   // float2 per in (or out) chunk buffer
@@ -104,14 +107,15 @@ cudaError_t prepare_kernel(size_t smem, int* occ) {
 }
 
 cudaError_t prepare_plan(tt_channel_s* h) {
-    // largest R whose double-buffered plan fits two CTAs per SM; else the generic kernel
+    // largest R whose two-stage pipeline fits one CTA per SM; else the generic kernel
     const int Rs[3] = {8, 4, 2};
     h->plan = Plan{};
     for (int i = 0; i < 3; ++i) {
         int nk = 0;
-        const size_t sm = smem_bytes(Rs[i], h->H, h->L, h->Lp, h->S, &nk);
+        const size_t sm = smem_bytes(Rs[i], 2, h->H, h->L, h->L4, h->S, &nk);
         if (sm <= kSmemBudget) {
             h->plan.R = Rs[i];
+            h->plan.stages = 2;
             h->plan.smem = sm;
             h->plan.nk_max = nk;
             break;
@@ -149,28 +153,36 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     p.hist_rd = h->hist + h->p * hs;
     p.hist_wr = h->hist + (1 - h->p) * hs;
     p.ring = h->ring;
-    p.dsort = h->dsort;
-    p.perm = h->perm;
+    p.xoff = h->xoff;
     p.n = n;
     p.t = h->t;
     p.cap = h->cap;
     p.chan_offset = h->chan_off;
     p.c_lo = c_lo;
     p.L = h->L;
-    p.Lp = h->Lp;
+    p.L4 = h->L4;
     p.H = h->H;
     p.S = h->S;
     p.key0 = static_cast<uint32_t>(h->seed);
     p.key1 = static_cast<uint32_t>(h->seed >> 32);
     // docs/tt-normal-v1.md §3: sigma / sqrt(2) rounded once in double, then to float
     p.noise_sc = static_cast<float>(static_cast<double>(sigma) * 0x1.6a09e667f3bcdp-1);
+    p.s_shift = -1;
+    if ((h->S & (h->S - 1)) == 0) {
+        p.s_shift = 0;
+        while ((1 << p.s_shift) < h->S) ++p.s_shift;
+    }
+    p.inv_S = static_cast<float>(1.0 / h->S);
+    p.t_div = h->t / h->S;
+    p.t_mod = static_cast<int32_t>(h->t % h->S);
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
     if (h->plan.R != 0) {
-        const int T = tt::kThreads * h->plan.R;
+        const int T = tt::kConsumerWarps * 32 * h->plan.R;
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
         p.nk_max = h->plan.nk_max;
+        p.stages = h->plan.stages;
         const int occ = noise ? h->occ[1] : h->occ[0];
         const int64_t grid = std::min<int64_t>(p.total_tiles, static_cast<int64_t>(h->num_sms) * occ);
         const dim3 g(static_cast<unsigned>(grid)), b(tt::kThreads);
@@ -187,11 +199,11 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         p.tiles_per_ch = 1;
         p.total_tiles = nch;
         const int64_t N = static_cast<int64_t>(nch) * n;
-        const int64_t grid = std::min<int64_t>((N + tt::kThreads - 1) / tt::kThreads, int64_t(h->num_sms) * 8);
+        const int64_t grid = std::min<int64_t>((N + 255) / 256, int64_t(h->num_sms) * 8);
         if (noise)
-            tt::tt_conv_generic_kernel<true><<<static_cast<unsigned>(grid), tt::kThreads, 0, st>>>(p);
+            tt::tt_conv_generic_kernel<true><<<static_cast<unsigned>(grid), 256, 0, st>>>(p);
         else
-            tt::tt_conv_generic_kernel<false><<<static_cast<unsigned>(grid), tt::kThreads, 0, st>>>(p);
+            tt::tt_conv_generic_kernel<false><<<static_cast<unsigned>(grid), 256, 0, st>>>(p);
         if (h->H > 0) {
             const int64_t tot = static_cast<int64_t>(nch) * h->H;
             const int64_t hg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);
@@ -207,6 +219,7 @@ tt_status check_apply(tt_channel_s* h, const void* in, const void* out, int64_t 
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
     if (!in || !out) return fail(TT_ERR_INVALID_ARG, "NULL in/out");
     if (n <= 0) return fail(TT_ERR_INVALID_ARG, "n_samples must be > 0 (got %lld)", (long long)n);
+    if (n > (int64_t(1) << 30)) return fail(TT_ERR_INVALID_ARG, "n_samples must be <= 2^30 per call (got %lld)", (long long)n);
     if (in == out) return fail(TT_ERR_INVALID_ARG, "in and out must not overlap");
     if (!(sigma >= 0.0f) || !std::isfinite(sigma)) return fail(TT_ERR_INVALID_ARG, "noise_sigma must be finite and >= 0");
     const int64_t k_lo = h->t / h->S;
@@ -220,8 +233,9 @@ tt_status check_apply(tt_channel_s* h, const void* in, const void* out, int64_t 
 void free_all(tt_channel_s* h) {
     cudaFree(h->ring);
     cudaFree(h->hist);
-    cudaFree(h->dsort);
     cudaFree(h->perm);
+    cudaFree(h->xoff);
+    cudaFree(h->load_stage);
     cudaFree(h->stage);
     for (int i = 0; i < 3; ++i) {
         if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
@@ -283,7 +297,7 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     h->num_sms = prop.multiProcessorCount;
     h->C = num_ue;
     h->L = num_taps;
-    h->Lp = (num_taps + 1) & ~1;
+    h->L4 = (num_taps + 1 + 3) & ~3;  // >= L + 1: room for the kernel's next-group prefetch
     h->S = snapshot_period;
     h->maxD = maxD;
     h->H = (maxD + 1) & ~1;
@@ -291,14 +305,15 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     h->cap = snapshot_capacity;
     h->chan_off = channel_offset;
 
-    // sorted-by-delay tap order per channel (stable: ties keep tap index order)
-    std::vector<int32_t> ds(CL), pm(CL);
+    // per channel: taps sorted by delay (stable: ties keep tap index order); perm[c][j]
+    // is the original index of sorted tap j, xoff[c][j] its window offset H - d
+    std::vector<int32_t> pm(static_cast<size_t>(CL)), xo(static_cast<size_t>(num_ue) * h->L4, 0);
     for (int c = 0; c < num_ue; ++c) {
-        int32_t* pc = pm.data() + static_cast<int64_t>(c) * num_taps;
+        int32_t* pc = pm.data() + static_cast<size_t>(c) * num_taps;
         std::iota(pc, pc + num_taps, 0);
         const int32_t* dc = delays + static_cast<int64_t>(c) * num_taps;
         std::stable_sort(pc, pc + num_taps, [dc](int32_t a, int32_t b) { return dc[a] < dc[b]; });
-        for (int j = 0; j < num_taps; ++j) ds[static_cast<int64_t>(c) * num_taps + j] = dc[pc[j]];
+        for (int j = 0; j < num_taps; ++j) xo[static_cast<size_t>(c) * h->L4 + j] = h->H - dc[pc[j]];
     }
     auto bail = [&](tt_status s) {
         free_all(h);
@@ -306,16 +321,16 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
         return s;
     };
     cudaError_t e;
-    const size_t ring_b = static_cast<size_t>(num_ue) * snapshot_capacity * h->Lp * sizeof(float2);
+    const size_t ring_b = static_cast<size_t>(num_ue) * snapshot_capacity * num_taps * sizeof(float4);
     const size_t hist_b = 2 * static_cast<size_t>(num_ue) * h->H * sizeof(float2);
-    const size_t tab_b = static_cast<size_t>(CL) * sizeof(int32_t);
+    const size_t pm_b = pm.size() * sizeof(int32_t), xo_b = xo.size() * sizeof(int32_t);
     if ((e = cudaMalloc(&h->ring, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(snapshot ring)"));
     if (hist_b && (e = cudaMalloc(&h->hist, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(history)"));
-    if ((e = cudaMalloc(&h->dsort, tab_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(delays)"));
-    if ((e = cudaMalloc(&h->perm, tab_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
-    h->dev_bytes = ring_b + hist_b + 2 * tab_b;
-    if ((e = cudaMemcpy(h->dsort, ds.data(), tab_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy delays"));
-    if ((e = cudaMemcpy(h->perm, pm.data(), tab_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
+    if ((e = cudaMalloc(&h->perm, pm_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
+    if ((e = cudaMalloc(&h->xoff, xo_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(xoff)"));
+    h->dev_bytes = ring_b + hist_b + pm_b + xo_b;
+    if ((e = cudaMemcpy(h->perm, pm.data(), pm_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
+    if ((e = cudaMemcpy(h->xoff, xo.data(), xo_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy xoff"));
     if (hist_b && (e = cudaMemset(h->hist, 0, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "zero history"));
     // the ring is zeroed so a never-loaded slot can never inject NaN into a CTA's
     // table (apply refuses non-resident ranges anyway)
@@ -334,26 +349,34 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
     if (count > h->cap) return fail(TT_ERR_INVALID_ARG, "count %lld exceeds snapshot_capacity %lld", (long long)count, (long long)h->cap);
     DeviceGuard dg(h->dev);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // [C][count][L] float2 (pitch L) -> ring [C][cap][Lp] at slots (first + i) mod cap:
-    // one 3-D pitched copy per contiguous slot range (at most two)
-    int64_t done = 0;
-    while (done < count) {
-        const int64_t k = first_index + done;
-        const int64_t slot = k % h->cap;
-        const int64_t m = std::min(count - done, h->cap - slot);
-        cudaMemcpy3DParms cp{};
-        cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(gains), static_cast<size_t>(h->L) * sizeof(float2),
-                                        static_cast<size_t>(h->L), static_cast<size_t>(count));
-        cp.srcPos = make_cudaPos(0, static_cast<size_t>(done), 0);
-        cp.dstPtr = make_cudaPitchedPtr(h->ring, static_cast<size_t>(h->Lp) * sizeof(float2), static_cast<size_t>(h->Lp),
-                                        static_cast<size_t>(h->cap));
-        cp.dstPos = make_cudaPos(0, static_cast<size_t>(slot), 0);
-        cp.extent = make_cudaExtent(static_cast<size_t>(h->L) * sizeof(float2), static_cast<size_t>(m),
-                                    static_cast<size_t>(h->C));
-        cp.kind = cudaMemcpyDefault;
-        TT_CUDA(cudaMemcpy3DAsync(&cp, st), "snapshot copy");
-        done += m;
+    // the loader kernel reads device memory; a host source goes through device staging
+    cudaPointerAttributes attr{};
+    cudaError_t pe = cudaPointerGetAttributes(&attr, gains);
+    if (pe != cudaSuccess) cudaGetLastError();
+    const bool on_device = pe == cudaSuccess && (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
+    const size_t elems = static_cast<size_t>(h->C) * count * h->L;
+    const float2* src = reinterpret_cast<const float2*>(gains);
+    if (!on_device) {
+        if (elems > h->load_stage_elems) {
+            TT_CUDA(cudaStreamSynchronize(st), "staging drain");
+            cudaFree(h->load_stage);
+            h->load_stage = nullptr;
+            h->load_stage_elems = 0;
+            TT_CUDA(cudaMalloc(&h->load_stage, elems * sizeof(float2)), "cudaMalloc(snapshot staging)");
+            h->load_stage_elems = elems;
+        }
+        TT_CUDA(cudaMemcpyAsync(h->load_stage, gains, elems * sizeof(float2), cudaMemcpyHostToDevice, st), "snapshot H2D");
+        src = h->load_stage;
     }
+    // snapshot first - 1 gets its difference now if it is resident and stays resident
+    const int fix_prev = (h->res_hi > h->res_lo && first_index - 1 >= h->res_lo && first_index - 1 < h->res_hi &&
+                          count <= h->cap - 1)
+                             ? 1
+                             : 0;
+    const int64_t grid = std::min<int64_t>((static_cast<int64_t>(elems) + 255) / 256, int64_t(h->num_sms) * 16);
+    tt::tt_load_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), 256, 0, st>>>(
+        src, count, first_index, h->ring, h->cap, h->perm, h->C, h->L, fix_prev);
+    TT_CUDA(cudaGetLastError(), "snapshot loader launch");
     const int64_t lo = first_index, hi = first_index + count;
     if (h->res_hi > h->res_lo && lo >= h->res_lo && lo <= h->res_hi) {
         h->res_hi = std::max(h->res_hi, hi);
@@ -467,7 +490,8 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->resident_hi = h->res_hi;
     info->channel_offset = h->chan_off;
     info->seed = h->seed;
-    info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2));
+    info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2) +
+                                              h->load_stage_elems * sizeof(float2));
     info->outputs_per_thread = h->plan.R;
     info->launches_per_apply = h->plan.R != 0 ? 1 : (h->H > 0 ? 2 : 1);
     return TT_OK;

@@ -4,24 +4,29 @@
 //   y_c[n] = sum_l (g_{c,l,k} + alpha (g_{c,l,k+1} - g_{c,l,k})) x_c[n - d_{c,l}] + w_c[n]
 //
 // Design:
-//  * persistent CTAs (grid = SMs x resident CTAs) walk a flat list of (channel, tile)
-//    work items; a tile is T = 256 R consecutive outputs of one channel;
-//  * each tile's input window x[i0 - H, i0 + T) (H = max-delay halo) and its raw gain
-//    snapshots are staged into shared memory by 1-D TMA bulk copies
-//    (cp.async.bulk ... mbarrier::complete_tx) into a double buffer, so the next
-//    tile's bytes are in flight while this tile computes; the halo before the call
-//    start comes from the carried delay-line history;
-//  * the snapshot pair of every interval the tile touches becomes a table of
-//    (g_k, g_{k+1} - g_k) float4 in tap order sorted by delay;
-//  * lane-interleaved outputs: lane j of warp w owns outputs w*32R + r*32 + j, so every
-//    x read is a conflict-free 256-B warp access; the warp's 32R outputs normally sit
-//    in one snapshot interval, making the coefficient read a broadcast;
-//  * per output-tap: h = fma(alpha, dg, g) then two packed FMAs (FFMA2, sm_100) into
-//    split accumulators A += h_re x, B += h_im x; y = (A.re - B.im, A.im + B.re);
+//  * data layout in HBM: the snapshot ring holds, per channel and snapshot k, one
+//    float4 (g_k, g_{k+1} - g_k) per tap, taps sorted by delay — written once by
+//    tt_load_kernel when snapshots are loaded — so a tile's coefficients are a
+//    contiguous, directly stageable block;
+//  * persistent, warp-specialised CTAs (one per SM): a producer warp walks the CTA's
+//    (channel, tile) work items and stages everything a tile reads — the input window
+//    x[i0 - H, i0 + T) (H = max-delay halo; the part before the call start comes from
+//    the carried delay line), the coefficient rows of the intervals it touches, and
+//    the channel's tap offsets H - d — into a ring of shared-memory stages with 1-D TMA
+//    bulk copies (cp.async.bulk ... mbarrier::complete_tx); 16 consumer warps wait on
+//    the stage's `full` mbarrier, compute, and release it on its `empty` mbarrier.
+//    There is no CTA-wide barrier in the steady state;
+//  * a tile is T = 16 warps x 32 lanes x R outputs of one channel; lane j of consumer
+//    warp w owns outputs w*32R + r*32 + j, so every x read is a conflict-free 256-B
+//    warp access and the warp's 32R outputs normally sit in one snapshot interval,
+//    making the coefficient read a broadcast;
+//  * taps run in groups of four with the next group's offsets prefetched; per tap the R
+//    gains h = fma(alpha, dg, g) are formed first (FFMA2), then two packed FMAs per
+//    output into split accumulators A += h_re x, B += h_im x; y = (A.re - B.im, A.im + B.re);
 //  * optional AWGN (docs/tt-normal-v1.md) fused in the epilogue, one Philox call per
 //    sample pair shared by neighbouring lanes via a shuffle;
-//  * the CTA that owns a channel's last tile writes the new delay-line history from
-//    its staged window into the other half of a ping-pong buffer.
+//  * the consumer warps of a channel's last tile write the new delay-line history from
+//    the staged window into the other half of a ping-pong buffer.
 //
 // Every output's operation sequence depends only on (channel, global n) — never on
 // the tile, path or launch shape — so results are bit-identical across partitions.
@@ -33,28 +38,33 @@
 
 namespace tt {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kConsumerWarps = 16;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+constexpr int kMaxStages = 4;
 
 struct ConvParams {
     const float2* x;        // [C_launch][n]: row 0 = channel c_lo
     float2* y;              // [C_launch][n]
     const float2* hist_rd;  // [C][H]  last H samples of the stream so far
     float2* hist_wr;        // [C][H]  written with the new history
-    const float2* ring;     // [C][cap][Lp] raw gain snapshots, original tap order
-    const int32_t* dsort;   // [C][L] delays sorted ascending
-    const int32_t* perm;    // [C][L] original tap index of each sorted position
+    const float4* ring;     // [C][cap][L] (g_k, g_{k+1} - g_k), taps sorted by delay
+    const int32_t* xoff;    // [C][L4] window offset H - d_j of sorted tap j (pads: 0)
     int64_t n;              // samples per channel in this call
     int64_t t;              // global index of the call's first sample
     int64_t cap;            // ring slots per channel
     int64_t chan_offset;    // global id of channel 0 (noise key)
     int64_t total_tiles;    // (c_hi - c_lo) * tiles_per_ch
+    int64_t t_div;          // t / S
+    int32_t t_mod;          // t % S
     int32_t c_lo;           // first channel of this launch
     int32_t tiles_per_ch;
-    int32_t L, Lp, H, S;
+    int32_t L, L4, H, S;
     int32_t nk_max;         // max snapshot intervals a tile touches
+    int32_t stages;         // shared-memory pipeline depth (<= kMaxStages)
     uint32_t key0, key1;    // noise key
     float noise_sc;         // sigma / sqrt(2) as float; 0 = no noise
+    int32_t s_shift;        // log2(S) if S is a power of two, else -1
+    float inv_S;            // 1/S (exact when S is a power of two)
 };
 
 // ---------------------------------------------------------------------------------
@@ -72,6 +82,9 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
@@ -92,27 +105,40 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
-// Stage `count` float2 from global `src` to shared `dst`. Thread 0 issues one TMA bulk
-// copy for the 16-B aligned body; the other elements (misaligned head / odd tail, or
-// everything when src and dst disagree mod 16 B) are copied by plain loads spread over
-// the CTA. Returns (to thread 0) the TMA bytes it issued. Plain stores become visible
-// at the CTA's next __syncthreads; TMA bytes at the mbarrier.
-__device__ __forceinline__ uint32_t stage_copy(float2* dst, const float2* src, int32_t count, uint64_t* bar,
-                                               bool issue) {
-    if (count <= 0) return 0;
-    int32_t head = 0, body = 0;
-    const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = smem_u32(dst);
-    if (((sa ^ da) & 15u) == 0) {
-        head = (sa & 15u) ? 1 : 0;
-        body = (count - head) & ~1;
-        if (body < 2) body = 0;
+// A global -> shared copy of `bytes` (a multiple of 8) split into a TMA body that is
+// 16-B aligned at both ends and at most one 8-B element before / after it; a copy whose
+// ends cannot both be aligned is all plain (8-B loads).
+struct Piece {
+    const unsigned char* src;
+    unsigned char* dst;
+    uint32_t bytes;
+    uint32_t head, body;  // plain bytes before the body (0 or 8), TMA body bytes
+};
+__device__ __forceinline__ Piece make_piece(void* dst, const void* src, uint32_t bytes) {
+    Piece pc{static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst), bytes, 0u, 0u};
+    if (bytes == 0) return pc;
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
+    if (((sa ^ smem_u32(dst)) & 15u) != 0) return pc;
+    pc.head = (sa & 15u) ? 8u : 0u;
+    const uint32_t body = (bytes - pc.head) & ~15u;
+    pc.body = body >= 16u ? body : 0u;
+    if (pc.body == 0) pc.head = 0;
+    return pc;
+}
+// plain part of a piece, spread over the producer warp's lanes
+__device__ __forceinline__ void piece_plain(const Piece& pc, int lane) {
+    if (pc.body == 0) {
+        for (uint32_t o = 8u * lane; o < pc.bytes; o += 256u)
+            *reinterpret_cast<float2*>(pc.dst + o) = __ldg(reinterpret_cast<const float2*>(pc.src + o));
+    } else {
+        if (lane == 0 && pc.head) *reinterpret_cast<float2*>(pc.dst) = __ldg(reinterpret_cast<const float2*>(pc.src));
+        const uint32_t tail = pc.head + pc.body;
+        if (lane == 1 && tail < pc.bytes)
+            *reinterpret_cast<float2*>(pc.dst + tail) = __ldg(reinterpret_cast<const float2*>(pc.src + tail));
     }
-    if (body > 0 && issue) tma_load_1d(dst + head, src + head, static_cast<uint32_t>(body) * 8u, bar);
-    for (int32_t i = threadIdx.x; i < count; i += kThreads) {
-        if (i >= head && i < head + body) continue;
-        dst[i] = __ldg(src + i);
-    }
-    return static_cast<uint32_t>(body) * 8u;
+}
+__device__ __forceinline__ void piece_tma(const Piece& pc, uint64_t* bar) {
+    if (pc.body) tma_load_1d(pc.dst + pc.head, pc.src + pc.head, pc.body, bar);
 }
 
 struct TileInfo {
@@ -124,150 +150,120 @@ struct TileInfo {
     int32_t j0;     // (t + i0) - kb*S
 };
 
+// 32-bit index math only: w < 2^31 tiles, i0 < 2^31 samples per call; the global
+// start t enters through the host-precomputed t / S and t % S.
+__device__ __forceinline__ uint32_t div_S(const ConvParams& p, uint32_t v) {
+    return p.s_shift >= 0 ? (v >> p.s_shift) : v / static_cast<uint32_t>(p.S);
+}
+
 template <int R>
 __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int64_t w) {
-    constexpr int T = kThreads * R;
+    constexpr int T = kConsumerWarps * 32 * R;
     TileInfo ti;
-    const int64_t cl = w / p.tiles_per_ch;
-    const int64_t tl = w - cl * p.tiles_per_ch;
+    const uint32_t w32 = static_cast<uint32_t>(w);
+    const uint32_t cl = w32 / static_cast<uint32_t>(p.tiles_per_ch);
+    const uint32_t tl = w32 - cl * static_cast<uint32_t>(p.tiles_per_ch);
     ti.c = p.c_lo + static_cast<int32_t>(cl);
-    ti.i0 = tl * T;
+    ti.i0 = static_cast<int64_t>(tl) * T;
     const int64_t rem = p.n - ti.i0;
     ti.Tt = rem < T ? static_cast<int32_t>(rem) : T;
-    const int64_t g0 = p.t + ti.i0;
-    ti.kb = g0 / p.S;
-    ti.j0 = static_cast<int32_t>(g0 - ti.kb * p.S);
-    ti.nk = static_cast<int32_t>((g0 + ti.Tt - 1) / p.S - ti.kb) + 1;
+    const uint32_t u0 = static_cast<uint32_t>(p.t_mod) + static_cast<uint32_t>(ti.i0);  // (t + i0) - (t / S) S
+    const uint32_t q0 = div_S(p, u0);
+    ti.kb = p.t_div + q0;
+    ti.j0 = static_cast<int32_t>(u0 - q0 * static_cast<uint32_t>(p.S));
+    ti.nk = static_cast<int32_t>(div_S(p, static_cast<uint32_t>(ti.j0 + ti.Tt - 1))) + 1;
     return ti;
 }
 
-// Issue the staging of tile `w` into buffer b: window [i0 - H, i0 + Tt) and raw snapshot
-// rows kb .. kb + nk. All threads call it (plain-load remainders are cooperative).
+// One pipeline stage in shared memory: input window (H + T float2), coefficient rows
+// (nk_max x L float4), tap offsets (L4 int32). Every region is a multiple of 16 B.
+struct Stage {
+    float2* win;
+    float4* coef;
+    int32_t* xo;
+};
+
+// Producer warp: stage tile `w` and arm `full` (plain parts first, then the barrier,
+// then the TMA bodies).
 template <int R>
-__device__ __forceinline__ void issue_tile(const ConvParams& p, int64_t w, float2* win, float2* raw, uint64_t* bar) {
+__device__ __forceinline__ void produce_tile(const ConvParams& p, int64_t w, const Stage& st, uint64_t* full,
+                                             int lane) {
     const TileInfo ti = tile_info<R>(p, w);
-    const bool lead = threadIdx.x == 0;
-    uint32_t tx = 0;
-    // Thread 0 must announce the byte count before any copy can complete, so it
-    // first computes the TMA bytes of every piece (issue = false pass is pure math).
-    // To keep it simple and exact, thread 0 arms the barrier with the total it will
-    // issue below; stage_copy's decision is deterministic.
     const int32_t H = p.H;
     const int64_t lo = ti.i0 - H;
     const int64_t hi = ti.i0 + ti.Tt;
-    // piece A: history part, local [lo, min(0, hi)) -> hist index H + local
-    const int32_t nA = lo < 0 ? static_cast<int32_t>((hi < 0 ? hi : 0) - lo) : 0;
-    const float2* srcA = p.hist_rd + static_cast<int64_t>(ti.c) * H + (H + lo);
-    // piece B: input part, local [max(lo, 0), hi)
+    // A: delay-line history, call-local [lo, min(0, hi)) -> history index H + local
+    const int64_t nA = lo < 0 ? ((hi < 0 ? hi : 0) - lo) : 0;
+    const Piece a = make_piece(st.win, p.hist_rd + static_cast<int64_t>(ti.c) * H + (H + lo),
+                               static_cast<uint32_t>(nA) * 8u);
+    // B: this call's input, call-local [max(lo, 0), hi)
     const int64_t bl = lo < 0 ? 0 : lo;
-    const int32_t nB = static_cast<int32_t>(hi - bl);
-    const float2* srcB = p.x + static_cast<int64_t>(ti.c - p.c_lo) * p.n + bl;
-    float2* dstB = win + (bl - lo);
-    // snapshot rows kb .. kb + nk (nk + 1 rows) from the ring, wrapping at cap
-    const int32_t rows = ti.nk + 1;
+    const Piece bx = make_piece(st.win + (bl - lo), p.x + static_cast<int64_t>(ti.c - p.c_lo) * p.n + bl,
+                                static_cast<uint32_t>(hi - bl) * 8u);
+    // C, D: coefficient rows kb .. kb + nk - 1, wrapping at the ring's capacity
     const int64_t s0 = ti.kb % p.cap;
-    const int32_t r1 = static_cast<int32_t>((p.cap - s0) < rows ? (p.cap - s0) : rows);
-    const float2* ringc = p.ring + static_cast<int64_t>(ti.c) * p.cap * p.Lp;
-    auto body_bytes = [](const float2* src, const float2* dst, int32_t count) -> uint32_t {
-        if (count <= 0) return 0;
-        const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
-        const uint32_t da = smem_u32(dst);
-        if (((sa ^ da) & 15u) != 0) return 0;
-        const int32_t head = (sa & 15u) ? 1 : 0;
-        int32_t body = (count - head) & ~1;
-        return body < 2 ? 0u : static_cast<uint32_t>(body) * 8u;
-    };
-    if (lead) {
-        tx = body_bytes(srcA, win, nA) + body_bytes(srcB, dstB, nB) +
-             body_bytes(ringc + s0 * p.Lp, raw, r1 * p.Lp) +
-             body_bytes(ringc, raw + static_cast<int64_t>(r1) * p.Lp, (rows - r1) * p.Lp);
-        mbar_arrive_expect_tx(bar, tx);
+    const int32_t r1 = static_cast<int32_t>((p.cap - s0) < ti.nk ? (p.cap - s0) : ti.nk);
+    const float4* ringc = p.ring + static_cast<int64_t>(ti.c) * p.cap * p.L;
+    const uint32_t rowb = static_cast<uint32_t>(p.L) * 16u;
+    const Piece c1 = make_piece(st.coef, ringc + s0 * p.L, static_cast<uint32_t>(r1) * rowb);
+    const Piece c2 = make_piece(st.coef + static_cast<int64_t>(r1) * p.L, ringc,
+                                static_cast<uint32_t>(ti.nk - r1) * rowb);
+    // E: tap offsets of this channel
+    const Piece e = make_piece(st.xo, p.xoff + static_cast<int64_t>(ti.c) * p.L4, static_cast<uint32_t>(p.L4) * 4u);
+    piece_plain(a, lane);
+    piece_plain(bx, lane);
+    piece_plain(c1, lane);
+    piece_plain(c2, lane);
+    piece_plain(e, lane);
+    __syncwarp();  // the lanes' plain stores happen-before lane 0's release (arrive)
+    if (lane == 0) {
+        mbar_arrive_expect_tx(full, a.body + bx.body + c1.body + c2.body + e.body);
+        piece_tma(a, full);
+        piece_tma(bx, full);
+        piece_tma(c1, full);
+        piece_tma(c2, full);
+        piece_tma(e, full);
     }
-    stage_copy(win, srcA, nA, bar, lead);
-    stage_copy(dstB, srcB, nB, bar, lead);
-    stage_copy(raw, ringc + s0 * p.Lp, r1 * p.Lp, bar, lead);
-    stage_copy(raw + static_cast<int64_t>(r1) * p.Lp, ringc, (rows - r1) * p.Lp, bar, lead);
 }
 
-// One tap of the output-tap loop for the R outputs a lane owns (rows r of its warp).
+// One tap for the R outputs this lane owns: gains first, then the packed MACs.
 template <int R>
 __device__ __forceinline__ void mac_tap(const float4 q, const float2* __restrict__ xp, const float (&alpha)[R],
                                         float2 (&A)[R], float2 (&B)[R]) {
+    float2 xv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
     const float2 g = make_float2(q.x, q.y);
     const float2 dg = make_float2(q.z, q.w);
+    float2 h[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) h[r] = __ffma2_rn(make_float2(alpha[r], alpha[r]), dg, g);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const float2 xv = xp[r * 32];
-        const float2 h = __ffma2_rn(make_float2(alpha[r], alpha[r]), dg, g);
-        A[r] = __ffma2_rn(make_float2(h.x, h.x), xv, A[r]);
-        B[r] = __ffma2_rn(make_float2(h.y, h.y), xv, B[r]);
+        A[r] = __ffma2_rn(make_float2(h[r].x, h[r].x), xv[r], A[r]);
+        B[r] = __ffma2_rn(make_float2(h[r].y, h[r].y), xv[r], B[r]);
     }
 }
 
+// Consumer warp: the 32R outputs of warp `cw` in tile `ti`.
 template <int R, bool NOISE>
-__global__ void __launch_bounds__(kThreads, 2) tt_conv_kernel(const ConvParams p) {
-    constexpr int T = kThreads * R;
-    extern __shared__ __align__(128) unsigned char smem[];
-    // layout: [bar 2 x 8 B][pad to 128][win 2 x (H+T) float2][raw 2 x RAW float2][coef nk_max x L float4][dl L int]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    const int32_t W = p.H + T;
-    const int32_t RAW = (p.nk_max + 1) * p.Lp;
-    float2* win0 = reinterpret_cast<float2*>(smem + 128);
-    float2* raw0 = win0 + 2 * W;
-    float4* coef = reinterpret_cast<float4*>(raw0 + 2 * RAW);
-    int32_t* dl = reinterpret_cast<int32_t*>(coef + static_cast<int64_t>(p.nk_max) * p.L);
-
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t phase = 0u;  // bit b = parity of buffer b's next completion
-    int b = 0;
-    int64_t w = blockIdx.x;
-    if (w < p.total_tiles) issue_tile<R>(p, w, win0, raw0, &bar[0]);
-
-    for (; w < p.total_tiles; w += gridDim.x, b ^= 1) {
-        const int64_t wn = w + gridDim.x;
-        if (wn < p.total_tiles) issue_tile<R>(p, wn, win0 + (b ^ 1) * W, raw0 + (b ^ 1) * RAW, &bar[b ^ 1]);
-        const TileInfo ti = tile_info<R>(p, w);
-        float2* win = win0 + b * W;
-        const float2* raw = raw0 + b * RAW;
-        mbar_wait(&bar[b], (phase >> b) & 1u);
-        phase ^= 1u << b;
-        __syncthreads();  // plain-load remainders of this buffer are visible
-
-        // coefficient table in sorted-tap order: coef[kk][j] = (g_k, g_{k+1} - g_k)
-        {
-            const int32_t* permc = p.perm + static_cast<int64_t>(ti.c) * p.L;
-            const int32_t* dc = p.dsort + static_cast<int64_t>(ti.c) * p.L;
-            const int32_t tot = ti.nk * p.L;
-            for (int32_t e = threadIdx.x; e < tot; e += kThreads) {
-                const int32_t kk = e / p.L, j = e - kk * p.L;
-                const int32_t src = __ldg(permc + j);
-                const float2 g0 = raw[kk * p.Lp + src];
-                const float2 g1 = raw[(kk + 1) * p.Lp + src];
-                coef[e] = make_float4(g0.x, g0.y, __fsub_rn(g1.x, g0.x), __fsub_rn(g1.y, g0.y));
-            }
-            for (int32_t j = threadIdx.x; j < p.L; j += kThreads) dl[j] = __ldg(dc + j);
-        }
-        __syncthreads();
-
-        // per-output interpolation weight alpha = j / S and interval index
-        const int32_t obase = warp * 32 * R + lane;
+__device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
+                                             int lane) {
+    const int32_t obase = cw * 32 * R + lane;
+    if (cw * 32 * R < ti.Tt) {
+        // per-output interpolation weight alpha = j / S (a multiply when S is a power of
+        // two: then j * (1/S) is exact and equals the correctly rounded quotient)
         float alpha[R];
         int32_t kk[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t jj = static_cast<uint32_t>(ti.j0 + obase + r * 32);
-            const uint32_t k = jj / static_cast<uint32_t>(p.S);
+            const uint32_t k = div_S(p, jj);
             // outputs past a tail tile's end are computed but never stored; keep their
-            // coefficient row inside the table
+            // coefficient row inside the staged block
             kk[r] = min(static_cast<int32_t>(k), ti.nk - 1);
-            alpha[r] = __fdiv_rn(__uint2float_rn(jj - k * static_cast<uint32_t>(p.S)), __int2float_rn(p.S));
+            const float jf = __uint2float_rn(jj - k * static_cast<uint32_t>(p.S));
+            alpha[r] = p.s_shift >= 0 ? __fmul_rn(jf, p.inv_S) : __fdiv_rn(jf, __int2float_rn(p.S));
         }
         float2 A[R], B[R];
 #pragma unroll
@@ -275,23 +271,32 @@ __global__ void __launch_bounds__(kThreads, 2) tt_conv_kernel(const ConvParams p
             A[r] = make_float2(0.f, 0.f);
             B[r] = make_float2(0.f, 0.f);
         }
-        const float2* xb = win + p.H + obase;
+        const float2* xb = st.win + obase;
         // warp-uniform: are all 32R outputs of this warp in one snapshot interval?
-        const uint32_t wj0 = static_cast<uint32_t>(ti.j0 + warp * 32 * R);
-        const bool uniform = (wj0 / static_cast<uint32_t>(p.S)) ==
-                             ((wj0 + 32 * R - 1) / static_cast<uint32_t>(p.S));
-        if (warp * 32 * R >= ti.Tt) {
-            // whole warp past the tail: nothing to compute
-        } else if (uniform) {
-            const float4* cf = coef + static_cast<int64_t>(wj0 / static_cast<uint32_t>(p.S)) * p.L;
-#pragma unroll 2
-            for (int32_t j = 0; j < p.L; ++j) mac_tap<R>(cf[j], xb - dl[j], alpha, A, B);
+        const uint32_t wj0 = static_cast<uint32_t>(ti.j0 + cw * 32 * R);
+        const uint32_t kw0 = div_S(p, wj0);
+        const uint32_t kw1 = div_S(p, wj0 + 32 * R - 1);
+        if (kw0 == kw1) {
+            const float4* cf = st.coef + static_cast<int64_t>(kw0) * p.L;
+            const int4* xo4 = reinterpret_cast<const int4*>(st.xo);
+            int32_t j = 0;
+            int4 o4 = xo4[0];
+            for (; j + 4 <= p.L; j += 4) {
+                const int4 o = o4;
+                o4 = xo4[(j >> 2) + 1];  // next group's offsets (L4 >= L + 1 keeps this in range)
+                const float4 q0 = cf[j], q1 = cf[j + 1], q2 = cf[j + 2], q3 = cf[j + 3];
+                mac_tap<R>(q0, xb + o.x, alpha, A, B);
+                mac_tap<R>(q1, xb + o.y, alpha, A, B);
+                mac_tap<R>(q2, xb + o.z, alpha, A, B);
+                mac_tap<R>(q3, xb + o.w, alpha, A, B);
+            }
+            for (; j < p.L; ++j) mac_tap<R>(cf[j], xb + st.xo[j], alpha, A, B);
         } else {
             for (int32_t j = 0; j < p.L; ++j) {
-                const float2* xp = xb - dl[j];
+                const float2* xp = xb + st.xo[j];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const float4 q = coef[kk[r] * p.L + j];
+                    const float4 q = st.coef[kk[r] * p.L + j];
                     const float2 xv = xp[r * 32];
                     const float2 h =
                         __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w), make_float2(q.x, q.y));
@@ -320,8 +325,9 @@ __global__ void __launch_bounds__(kThreads, 2) tt_conv_kernel(const ConvParams p
                     const uint32_t s0 = ev ? q.c : q.a, s1 = ev ? q.d : q.b;
                     const uint32_t v0 = __shfl_xor_sync(0xffffffffu, s0, 1);
                     const uint32_t v1 = __shfl_xor_sync(0xffffffffu, s1, 1);
-                    const float2 wa = ev ? noise_from_words(q.a, q.b, p.noise_sc) : noise_from_words(v0, v1, p.noise_sc);
-                    const float2 wb = ev ? noise_from_words(v0, v1, p.noise_sc) : noise_from_words(q.c, q.d, p.noise_sc);
+                    // select the words first so each lane runs the transform once per sample
+                    const float2 wa = noise_from_words(ev ? q.a : v0, ev ? q.b : v1, p.noise_sc);
+                    const float2 wb = noise_from_words(ev ? v0 : q.c, ev ? v1 : q.d, p.noise_sc);
                     out[r] = make_float2(__fadd_rn(out[r].x, wa.x), __fadd_rn(out[r].y, wa.y));
                     out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, wb.x), __fadd_rn(out[r + 1].y, wb.y));
                 }
@@ -332,8 +338,8 @@ __global__ void __launch_bounds__(kThreads, 2) tt_conv_kernel(const ConvParams p
                     const uint64_t m = static_cast<uint64_t>(n) >> 1;
                     const u32x4 q = philox4x32_10(static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32), cg, 0u,
                                                   p.key0, p.key1);
-                    const float2 wv = (n & 1) ? noise_from_words(q.c, q.d, p.noise_sc)
-                                              : noise_from_words(q.a, q.b, p.noise_sc);
+                    const bool odd = (n & 1) != 0;
+                    const float2 wv = noise_from_words(odd ? q.c : q.a, odd ? q.d : q.b, p.noise_sc);
                     out[r] = make_float2(__fadd_rn(out[r].x, wv.x), __fadd_rn(out[r].y, wv.y));
                 }
             }
@@ -344,13 +350,64 @@ __global__ void __launch_bounds__(kThreads, 2) tt_conv_kernel(const ConvParams p
             const int32_t o = obase + r * 32;
             if (o < ti.Tt) yc[o] = out[r];
         }
-        // the tile that ends the call writes the new delay-line history (ping-pong)
-        if (ti.i0 + ti.Tt == p.n) {
-            float2* hw = p.hist_wr + static_cast<int64_t>(ti.c) * p.H;
-            const int32_t off = ti.Tt;  // window index of local sample n - H is (n - H) - (i0 - H) = Tt
-            for (int32_t i = threadIdx.x; i < p.H; i += kThreads) hw[i] = win[off + i];
+    }
+    // the tile that ends the call writes the new delay-line history (ping-pong); the
+    // window index of call-local sample n - H + i is Tt + i
+    if (ti.i0 + ti.Tt == p.n) {
+        float2* hw = p.hist_wr + static_cast<int64_t>(ti.c) * p.H;
+        for (int32_t i = cw * 32 + lane; i < p.H; i += kConsumerWarps * 32) hw[i] = st.win[ti.Tt + i];
+    }
+}
+
+template <int R, bool NOISE>
+__global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p) {
+    constexpr int T = kConsumerWarps * 32 * R;
+    extern __shared__ __align__(128) unsigned char smem[];
+    // layout: [full kMaxStages x 8 B | empty kMaxStages x 8 B | pad to 128][stage 0][stage 1]...
+    //   stage = [win (H+T) float2][coef nk_max x L float4][xo L4 int32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kMaxStages;
+    const int64_t WB = static_cast<int64_t>(p.H + T) * 8;
+    const int64_t CB = static_cast<int64_t>(p.nk_max) * p.L * 16;
+    const int64_t SB = WB + CB + static_cast<int64_t>(p.L4) * 4;
+    auto stage = [&](int s) {
+        unsigned char* base = smem + 128 + s * SB;
+        Stage st;
+        st.win = reinterpret_cast<float2*>(base);
+        st.coef = reinterpret_cast<float4*>(base + WB);
+        st.xo = reinterpret_cast<int32_t*>(base + WB + CB);
+        return st;
+    };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
         }
-        __syncthreads();  // buffer b, coef and dl are free for reuse
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // producer: run ahead of the consumers by up to `stages` tiles
+        int it = 0;
+        for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
+            const int s = it % p.stages;
+            const int k = it / p.stages;
+            if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
+            produce_tile<R>(p, w, stage(s), &full[s], lane);
+        }
+    } else {
+        int it = 0;
+        for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
+            const int s = it % p.stages;
+            const int k = it / p.stages;
+            mbar_wait(&full[s], k & 1);
+            const TileInfo ti = tile_info<R>(p, w);
+            consume_tile<R, NOISE>(p, ti, stage(s), warp, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     }
 }
 
@@ -358,11 +415,11 @@ __global__ void __launch_bounds__(kThreads, 2) tt_conv_kernel(const ConvParams p
 // when the tiled kernel's shared-memory plan does not fit (very long filters with very
 // short snapshot periods). Same per-output operation sequence => bit-identical.
 template <bool NOISE>
-__global__ void __launch_bounds__(kThreads) tt_conv_generic_kernel(const ConvParams p) {
+__global__ void __launch_bounds__(256) tt_conv_generic_kernel(const ConvParams p) {
     const int64_t nch = p.total_tiles / p.tiles_per_ch;
     const int64_t N = nch * p.n;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; e < N;
-         e += static_cast<int64_t>(gridDim.x) * kThreads) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < N;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t cl = e / p.n;
         const int64_t i = e - cl * p.n;
         const int32_t c = p.c_lo + static_cast<int32_t>(cl);
@@ -370,19 +427,16 @@ __global__ void __launch_bounds__(kThreads) tt_conv_generic_kernel(const ConvPar
         const int64_t k = n / p.S;
         const int32_t jj = static_cast<int32_t>(n - k * p.S);
         const float alpha = __fdiv_rn(__uint2float_rn(static_cast<uint32_t>(jj)), __int2float_rn(p.S));
-        const float2* g0r = p.ring + (static_cast<int64_t>(c) * p.cap + (k % p.cap)) * p.Lp;
-        const float2* g1r = p.ring + (static_cast<int64_t>(c) * p.cap + ((k + 1) % p.cap)) * p.Lp;
+        const float4* cr = p.ring + (static_cast<int64_t>(c) * p.cap + (k % p.cap)) * p.L;
         const float2* xc = p.x + cl * p.n;
         const float2* hc = p.hist_rd + static_cast<int64_t>(c) * p.H;
+        const int32_t* xo = p.xoff + static_cast<int64_t>(c) * p.L4;
         float2 A = make_float2(0.f, 0.f), Bv = make_float2(0.f, 0.f);
         for (int32_t j = 0; j < p.L; ++j) {
-            const int32_t src = __ldg(p.perm + static_cast<int64_t>(c) * p.L + j);
-            const int32_t d = __ldg(p.dsort + static_cast<int64_t>(c) * p.L + j);
-            const float2 g0 = __ldg(g0r + src), g1 = __ldg(g1r + src);
-            const float2 dg = make_float2(__fsub_rn(g1.x, g0.x), __fsub_rn(g1.y, g0.y));
-            const int64_t m = i - d;
+            const float4 q = __ldg(cr + j);
+            const int64_t m = i - (p.H - __ldg(xo + j));
             const float2 xv = m >= 0 ? __ldg(xc + m) : __ldg(hc + (p.H + m));
-            const float2 h = __ffma2_rn(make_float2(alpha, alpha), dg, g0);
+            const float2 h = __ffma2_rn(make_float2(alpha, alpha), make_float2(q.z, q.w), make_float2(q.x, q.y));
             A = __ffma2_rn(make_float2(h.x, h.x), xv, A);
             Bv = __ffma2_rn(make_float2(h.y, h.y), xv, Bv);
         }
@@ -391,7 +445,8 @@ __global__ void __launch_bounds__(kThreads) tt_conv_generic_kernel(const ConvPar
             const uint64_t mm = static_cast<uint64_t>(n) >> 1;
             const u32x4 q = philox4x32_10(static_cast<uint32_t>(mm), static_cast<uint32_t>(mm >> 32),
                                           static_cast<uint32_t>(p.chan_offset + c), 0u, p.key0, p.key1);
-            const float2 wv = (n & 1) ? noise_from_words(q.c, q.d, p.noise_sc) : noise_from_words(q.a, q.b, p.noise_sc);
+            const bool odd = (n & 1) != 0;
+            const float2 wv = noise_from_words(odd ? q.c : q.a, odd ? q.d : q.b, p.noise_sc);
             o = make_float2(__fadd_rn(o.x, wv.x), __fadd_rn(o.y, wv.y));
         }
         p.y[cl * p.n + i] = o;
@@ -410,6 +465,38 @@ __global__ void tt_history_kernel(const ConvParams p, int32_t nch) {
         const int64_t m = p.n - p.H + i;  // call-local index of the sample
         p.hist_wr[static_cast<int64_t>(c) * p.H + i] =
             m >= 0 ? p.x[cl * p.n + m] : p.hist_rd[static_cast<int64_t>(c) * p.H + (p.H + m)];
+    }
+}
+
+// Snapshot loader (P:309 / P:411 trace ingestion): writes snapshots first .. first +
+// count - 1 of every channel into the ring as (g_k, g_{k+1} - g_k) in sorted-tap order.
+// src: device float2 [C][count][L] in the caller's (original) tap order; perm [C][L]:
+// original index of sorted tap j. The difference of the last new snapshot is completed
+// by the next contiguous load; `fix_prev` completes snapshot first - 1's difference.
+__global__ void tt_load_kernel(const float2* __restrict__ src, int64_t count, int64_t first, float4* ring, int64_t cap,
+                               const int32_t* __restrict__ perm, int32_t C, int32_t L, int32_t fix_prev) {
+    const int64_t tot = static_cast<int64_t>(C) * count * L;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t j = static_cast<int32_t>(e % L);
+        const int64_t ci = e / L;
+        const int64_t i = ci % count;
+        const int64_t c = ci / count;
+        const int32_t o = __ldg(perm + c * L + j);
+        const float2 g = __ldg(src + (c * count + i) * L + o);
+        float4 v = make_float4(g.x, g.y, 0.f, 0.f);
+        if (i + 1 < count) {
+            const float2 g1 = __ldg(src + (c * count + i + 1) * L + o);
+            v.z = __fsub_rn(g1.x, g.x);
+            v.w = __fsub_rn(g1.y, g.y);
+        }
+        const int64_t k = first + i;
+        ring[(c * cap + k % cap) * L + j] = v;
+        if (i == 0 && fix_prev) {
+            float4* pv = ring + (c * cap + (k - 1) % cap) * L + j;
+            pv->z = __fsub_rn(g.x, pv->x);
+            pv->w = __fsub_rn(g.y, pv->y);
+        }
     }
 }
 

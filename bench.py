@@ -146,23 +146,32 @@ def cpu_baseline(w: ttsynth.Workload, target_s: float = 10.0):
 
     cores = len(os.sched_getaffinity(0))
     n = w.n_per_call
-    chans, elapsed, done = 1, 0.0, 0
-    d_all = ttsynth.delays(w, 0, min(w.C, 4096))
-    while True:
-        c = min(chans, w.C)
-        K = (n - 1) // w.S + 2
-        g = ttsynth.snapshots(w, 0, c, K)
-        x = ttsynth.iq(w, 0, c, 0)
+    # probe: one slot of a few channels -> rate; then size (channels, consecutive slots)
+    # for ~target_s of oracle work on this workload
+    c0 = min(w.C, max(1, cores))
+    K = (n - 1) // w.S + 2
+    pd, pg, px = ttsynth.delays(w, 0, c0), ttsynth.snapshots(w, 0, c0, K), ttsynth.iq(w, 0, c0, 0)
+    best = float("inf")
+    for _ in range(2):  # the first call also pays library load / thread-pool start
         t0 = time.perf_counter()
-        oracle.convolve(d_all[:c], w.S, g, 0, x, 0, 0, n, sigma=w.sigma, seed=0)
-        dt = time.perf_counter() - t0
-        elapsed, done = dt, c * n
-        if dt >= target_s / 4 or c >= w.C or c >= 4096:
-            break
-        chans = min(w.C, max(c * 2, int(c * target_s / max(dt, 1e-3))))
+        oracle.convolve(pd, w.S, pg, 0, px, 0, 0, n, sigma=w.sigma, seed=0)
+        best = min(best, time.perf_counter() - t0)
+    rate = c0 * n / max(best, 1e-4)
+    want = rate * target_s
+    c = int(min(w.C, max(1, want // n)))
+    slots = int(min(w.calls, max(1, want // (c * n))))
+    N = slots * n
+    K = (N - 1) // w.S + 2
+    d = ttsynth.delays(w, 0, c)
+    g = ttsynth.snapshots(w, 0, c, K)
+    x = np.concatenate([ttsynth.iq(w, 0, c, i) for i in range(slots)], axis=1)
+    t0 = time.perf_counter()
+    oracle.convolve(d, w.S, g, 0, x, 0, 0, N, sigma=w.sigma, seed=0)
+    elapsed = time.perf_counter() - t0
+    done = c * N
     return {"value": done / elapsed, "unit": "samples/s", "cores": cores, "kind": "oracle",
-            "sample": f"{min(chans, w.C)} channels x 1 slot of {n} samples of {w.name} "
-                      f"({done} samples, {elapsed:.2f} s wall, double precision, OpenMP)"}
+            "sample": f"{c} of {w.C} channels x {slots} consecutive slots of {n} samples of {w.name} "
+                      f"({done} samples, {elapsed:.2f} s wall, double precision, OpenMP over {cores} threads)"}
 
 
 def run_reference(args, w):

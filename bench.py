@@ -104,10 +104,8 @@ class ClockSampler:
 
 
 def _dist():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def roofline(w: ttsynth.Workload, samples: int, kernel_s: float, peaks: dict, traffic):
@@ -244,22 +242,18 @@ def main():
 
     import torch
 
-    from paper_2601_08217_b200 import Channel
+    from paper_2601_08217_b200 import Channel, shard
 
-    rank, world, local = _dist()
+    rank, world, local = shard.env()
     if world != args.gpus and rank == 0:
         print(f"note: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
+    pg = shard.init("nccl", dev)
 
     # ---- this rank's shard (contiguous UE block; DL/UL of a UE stay together) ----------
-    c_lo, c_hi = ttsynth.shard_ues(w, rank, world)
+    c_lo, c_hi = shard.ue_block(w.ues, w.dirs, rank, world)
+    assert (c_lo, c_hi) == ttsynth.shard_ues(w, rank, world)
     C, n = c_hi - c_lo, w.n_per_call
     steps_total = args.warmup + args.steps + max(args.e2e_steps, 0) + 1
     K = (steps_total * n - 1) // w.S + 2
@@ -281,8 +275,7 @@ def main():
     for i in range(args.warmup):
         ch.apply(xs[i % P], out=y, noise_sigma=sigma)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    if pg:
-        pg.barrier()
+    shard.barrier(pg)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev[0].record(stream)
@@ -290,15 +283,10 @@ def main():
             ch.apply(xs[(args.warmup + i) % P], out=y, noise_sigma=sigma)
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
-    if pg:
-        pg.barrier()
+    shard.barrier(pg)
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]  # ms, one launch each
-    elapsed_ms = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if pg:
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-    elapsed_max = float(t.item())
-    samples_all = w.C * n * args.steps  # every rank's channels
+    elapsed_max = shard.max_over_ranks(ev[0].elapsed_time(ev[-1]), dev, pg)
+    samples_all = shard.sum_over_ranks(C * n * args.steps, dev, pg)  # units all ranks processed
     value = samples_all / (elapsed_max / 1e3)
     kernel_s = statistics.mean(per_step) / 1e3
 
@@ -309,18 +297,15 @@ def main():
         yh = torch.empty_like(xh[0]).pin_memory()
         ch.apply_host(xh[0], yh, noise_sigma=sigma)  # staging allocation + warm-up
         torch.cuda.synchronize()
-        if pg:
-            pg.barrier()
+        shard.barrier(pg)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.e2e_steps):
             ch.apply_host(xh[i % len(xh)], yh, noise_sigma=sigma)
         e1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if pg:
-            pg.all_reduce(te, op=pg.ReduceOp.MAX)
-        e2e = {"value": w.C * n * args.e2e_steps / (float(te.item()) / 1e3), "unit": "samples/s",
+        te = shard.max_over_ranks(e0.elapsed_time(e1), dev, pg)
+        e2e = {"value": shard.sum_over_ranks(C * n * args.e2e_steps, dev, pg) / (te / 1e3), "unit": "samples/s",
                "h2d_bytes_per_step": slot_bytes, "d2h_bytes_per_step": slot_bytes,
                "steps": args.e2e_steps, "api": "tt_channel_apply_host (pinned host buffers)"}
     info = ch.info()

@@ -113,6 +113,8 @@ def ue_delays(w: Workload, ue: int) -> np.ndarray:
 def delays(w: Workload, c_lo: int = 0, c_hi: Optional[int] = None) -> np.ndarray:
     """[c_hi - c_lo][L] int32 delays for GLOBAL channels c_lo..c_hi-1."""
     c_hi = w.C if c_hi is None else c_hi
+    if c_hi <= c_lo:
+        return np.zeros((0, w.L), dtype=np.int32)
     return np.stack([ue_delays(w, c // w.dirs) for c in range(c_lo, c_hi)]).astype(np.int32)
 
 

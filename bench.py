@@ -242,7 +242,7 @@ def main():
 
     import torch
 
-    from paper_2601_08217_b200 import Channel, shard
+    from paper_2601_08217_b200 import Channel, _lib, shard
 
     rank, world, local = shard.env()
     if world != args.gpus and rank == 0:
@@ -256,7 +256,11 @@ def main():
     assert (c_lo, c_hi) == ttsynth.shard_ues(w, rank, world)
     C, n = c_hi - c_lo, w.n_per_call
     steps_total = args.warmup + args.steps + max(args.e2e_steps, 0) + 1
-    K = (steps_total * n - 1) // w.S + 2
+    # streaming configs (c3, c4: many slots) carry the delay line from slot to slot; a
+    # one-call config (c1, c2, c5) repeats its single call, the stream reset (t = 0, zero
+    # delay line) inside each step
+    one_shot = w.calls == 1
+    K = (n - 1) // w.S + 2 if one_shot else (steps_total * n - 1) // w.S + 2
     delays = ttsynth.delays(w, c_lo, c_hi)
     gains = ttsynth.snapshots(w, c_lo, c_hi, K, backend="torch", device=dev)
     slot_bytes = C * n * 8
@@ -272,15 +276,20 @@ def main():
     sigma = w.sigma if args.sigma is None else args.sigma
 
     # ---- device-resident timed region ----------------------------------------------
+    def step(xin):
+        if one_shot:
+            ch.reset()
+        ch.apply(xin, out=y, noise_sigma=sigma)
+
     for i in range(args.warmup):
-        ch.apply(xs[i % P], out=y, noise_sigma=sigma)
+        step(xs[i % P])
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     shard.barrier(pg)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
-            ch.apply(xs[(args.warmup + i) % P], out=y, noise_sigma=sigma)
+            step(xs[(args.warmup + i) % P])
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
     shard.barrier(pg)
@@ -295,12 +304,16 @@ def main():
     if args.e2e_steps > 0:
         xh = [xs[i % P].cpu().pin_memory() for i in range(min(P, 2))]
         yh = torch.empty_like(xh[0]).pin_memory()
+        if one_shot:
+            ch.reset()
         ch.apply_host(xh[0], yh, noise_sigma=sigma)  # staging allocation + warm-up
         torch.cuda.synchronize()
         shard.barrier(pg)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.e2e_steps):
+            if one_shot:
+                ch.reset()
             ch.apply_host(xh[i % len(xh)], yh, noise_sigma=sigma)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -326,7 +339,8 @@ def main():
             "call_ms": {"p50": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
                         "slot_ms": 1e3 * n / w.rate_sps},
             "gpu_launches": args.steps * int(info.launches_per_apply),
-            "plan": {"outputs_per_thread": int(info.outputs_per_thread), "threads_per_cta": 256},
+            "plan": {"kernel": _lib.KERNELS.get(int(info.kernel), "?"),
+                     "outputs_per_thread": int(info.outputs_per_thread)},
             "clocks": clk.summary(),
             "e2e": e2e,
         }

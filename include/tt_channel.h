@@ -67,7 +67,7 @@ typedef struct {
     int32_t num_ue;            /* C: channel streams in this handle */
     int32_t num_taps;          /* L */
     int32_t snapshot_period;   /* S */
-    int32_t history;           /* H: delay-line samples kept per channel (max delay rounded up to even) */
+    int32_t history;           /* H: delay-line samples kept per channel = max delay rounded up to 16, + 16 */
     int32_t max_delay;         /* max over all d_{c,l} */
     int32_t device;            /* CUDA device the handle is bound to */
     int64_t t;                 /* global index of the next sample to be applied */
@@ -77,9 +77,17 @@ typedef struct {
     int64_t channel_offset;    /* global id of channel 0 (noise key) */
     uint64_t seed;             /* noise key */
     int64_t device_bytes;      /* device memory owned by the handle */
-    int32_t outputs_per_thread; /* tiled-kernel plan R (T = 256 R outputs per tile); 0 = generic kernel */
+    int32_t outputs_per_thread; /* outputs per thread of the selected kernel (0 = generic kernel) */
     int32_t launches_per_apply; /* kernel launches one tt_channel_apply enqueues */
+    int32_t kernel;             /* TT_KERNEL_* the plan selected */
 } tt_channel_info;
+
+/* kernels a plan can select (all compute the same per-output operation sequence, so
+ * their outputs are bit-identical; the environment variable TT_KERNEL=rw|tiled|generic
+ * read at create restricts the choice) */
+#define TT_KERNEL_GENERIC 0 /* one thread per output, operands from global memory */
+#define TT_KERNEL_TILED 1   /* TMA-staged tiles, lane-strided outputs, x from shared memory */
+#define TT_KERNEL_RW 2      /* register-window kernel: 16 consecutive outputs per thread */
 
 /* Create a handle for C = num_ue channels with L = num_taps taps each.
  *   delays: host int32 [C][L], each in [0, TT_MAX_DELAY]; duplicates allowed (the

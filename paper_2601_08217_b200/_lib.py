@@ -62,7 +62,11 @@ class ChannelInfo(ct.Structure):
         ("device_bytes", ct.c_int64),
         ("outputs_per_thread", ct.c_int32),
         ("launches_per_apply", ct.c_int32),
+        ("kernel", ct.c_int32),
     ]
+
+
+KERNELS = {0: "generic", 1: "tiled", 2: "rw"}
 
 
 _lock = threading.Lock()

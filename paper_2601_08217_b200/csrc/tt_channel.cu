@@ -8,12 +8,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
 
 #include "tt_channel.h"
 #include "tt_conv.cuh"
+#include "tt_conv_rw.cuh"
 
 namespace {
 
@@ -52,6 +54,8 @@ struct DeviceGuard {
 
 // Launch plan of the tiled kernel for one handle.
 struct Plan {
+    bool rw = false;     // register-window kernel (tt_conv_rw.cuh)
+    int rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
     int R = 0;           // outputs per consumer thread (0 = generic kernel)
     int stages = 0;      // shared-memory pipeline depth
     size_t smem = 0;     // dynamic shared memory bytes
@@ -84,6 +88,7 @@ struct tt_channel_s {
     float2* hist = nullptr;    // [2][C][H] delay-line ping-pong
     int32_t* perm = nullptr;   // [C][L] original tap index of sorted tap j
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
+    int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
     float2* load_stage = nullptr;  // device staging for host-memory snapshot sources
     size_t load_stage_elems = 0;
     size_t dev_bytes = 0;
@@ -107,10 +112,45 @@ cudaError_t prepare_kernel(size_t smem, int* occ) {
 }
 
 cudaError_t prepare_plan(tt_channel_s* h) {
+    h->plan = Plan{};
+    // TT_KERNEL=rw|tiled|generic restricts the choice (tests compare the paths bit for bit)
+    const char* force = getenv("TT_KERNEL");
+    const bool allow_rw = !force || !strcmp(force, "rw");
+    const bool allow_tiled = !force || !strcmp(force, "tiled") || !strcmp(force, "rw");
+    // register-window kernel: needs 16-aligned snapshot intervals and two window stages
+    // of (Hp + T) / 16 doubled blocks in shared memory
+    if (allow_rw && h->S % 16 == 0) {
+        const int Hp = h->H - 16;
+        const int nb = (Hp + tt::rw::T) / 16;
+        const size_t wbytes = (static_cast<size_t>(nb) * tt::rw::kBlockBytes + 15) & ~size_t(15);
+        const size_t rows = (tt::rw::T - 1) / h->S + 2;
+        const size_t row_stride = static_cast<size_t>(h->L) * 16 + 16;
+        const size_t tbytes = (static_cast<size_t>(h->L + 1) * 8 + 15) & ~size_t(15);
+        const size_t sbytes = wbytes + rows * row_stride + tbytes;
+        const size_t sm = 128 + 2 * sbytes;
+        if (sm <= 227 * 1024) {
+            h->plan.rw_wbytes = static_cast<int>(wbytes);
+            h->plan.rw_rows = static_cast<int>(rows);
+            h->plan.rw_row_stride = static_cast<int>(row_stride);
+            h->plan.rw_sbytes = static_cast<int>(sbytes);
+            h->plan.rw = true;
+            h->plan.R = tt::rw::R;
+            h->plan.stages = 2;
+            h->plan.smem = sm;
+            cudaError_t e;
+            if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sm))) != cudaSuccess)
+                return e;
+            if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sm))) != cudaSuccess)
+                return e;
+            h->occ[0] = h->occ[1] = 1;
+            return cudaSuccess;
+        }
+    }
     // largest R whose two-stage pipeline fits one CTA per SM; else the generic kernel
     const int Rs[3] = {8, 4, 2};
-    h->plan = Plan{};
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; allow_tiled && i < 3; ++i) {
         int nk = 0;
         const size_t sm = smem_bytes(Rs[i], 2, h->H, h->L, h->L4, h->S, &nk);
         if (sm <= kSmemBudget) {
@@ -177,7 +217,43 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     p.t_mod = static_cast<int32_t>(h->t % h->S);
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
-    if (h->plan.R != 0) {
+    if (h->plan.rw) {
+        tt::rw::Params q{};
+        q.x = x;
+        q.y = y;
+        q.hist_rd = p.hist_rd;
+        q.hist_wr = p.hist_wr;
+        q.ring = h->ring;
+        q.tab = h->tab;
+        q.n = n;
+        q.t = h->t;
+        q.cap = h->cap;
+        q.chan_offset = h->chan_off;
+        q.c_lo = c_lo;
+        q.L = h->L;
+        q.H = h->H;
+        q.Hp = h->H - 16;
+        q.S = h->S;
+        q.a = static_cast<int32_t>(h->t & 15);
+        q.nb = (q.Hp + tt::rw::T) / 16;
+        q.s_shift = p.s_shift;
+        q.inv_S = p.inv_S;
+        q.key0 = p.key0;
+        q.key1 = p.key1;
+        q.noise_sc = p.noise_sc;
+        q.vec_store = ((n & 1) == 0 && (q.a & 1) == 0) ? 1 : 0;
+        q.rows = h->plan.rw_rows;
+        q.row_stride = h->plan.rw_row_stride;
+        q.wbytes = h->plan.rw_wbytes;
+        q.sbytes = h->plan.rw_sbytes;
+        q.tiles_per_ch = static_cast<int32_t>((n + q.a + tt::rw::T - 1) / tt::rw::T);
+        q.total_tiles = static_cast<int64_t>(nch) * q.tiles_per_ch;
+        const int64_t grid = std::min<int64_t>(q.total_tiles, static_cast<int64_t>(h->num_sms));
+        if (noise)
+            tt::rw::tt_conv_rw_kernel<true><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.smem, st>>>(q);
+        else
+            tt::rw::tt_conv_rw_kernel<false><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.smem, st>>>(q);
+    } else if (h->plan.R != 0) {
         const int T = tt::kConsumerWarps * 32 * h->plan.R;
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
@@ -235,6 +311,7 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->hist);
     cudaFree(h->perm);
     cudaFree(h->xoff);
+    cudaFree(h->tab);
     cudaFree(h->load_stage);
     cudaFree(h->stage);
     for (int i = 0; i < 3; ++i) {
@@ -300,7 +377,7 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     h->L4 = (num_taps + 1 + 3) & ~3;  // >= L + 1: room for the kernel's next-group prefetch
     h->S = snapshot_period;
     h->maxD = maxD;
-    h->H = (maxD + 1) & ~1;
+    h->H = ((maxD + 15) & ~15) + 16;  // >= D + 16: a 16-aligned window start reaches back <= 15 more
     h->seed = seed;
     h->cap = snapshot_capacity;
     h->chan_off = channel_offset;
@@ -308,12 +385,22 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     // per channel: taps sorted by delay (stable: ties keep tap index order); perm[c][j]
     // is the original index of sorted tap j, xoff[c][j] its window offset H - d
     std::vector<int32_t> pm(static_cast<size_t>(CL)), xo(static_cast<size_t>(num_ue) * h->L4, 0);
+    // register-window table: per sorted tap, the byte offset of its window in a thread's
+    // doubled block ((o >> 4) blocks + (o & 15) slots, o = Hp - d) and the number of fresh
+    // samples min(d_j - d_{j-1}, 16) (16 for the first tap); entry L is padding
+    std::vector<int2> tb(static_cast<size_t>(num_ue) * (num_taps + 1), int2{0, 0});
     for (int c = 0; c < num_ue; ++c) {
         int32_t* pc = pm.data() + static_cast<size_t>(c) * num_taps;
         std::iota(pc, pc + num_taps, 0);
         const int32_t* dc = delays + static_cast<int64_t>(c) * num_taps;
         std::stable_sort(pc, pc + num_taps, [dc](int32_t a, int32_t b) { return dc[a] < dc[b]; });
         for (int j = 0; j < num_taps; ++j) xo[static_cast<size_t>(c) * h->L4 + j] = h->H - dc[pc[j]];
+        const int Hp = h->H - 16;
+        for (int j = 0; j < num_taps; ++j) {
+            const int o = Hp - dc[pc[j]];
+            const int gap = j == 0 ? 16 : std::min(16, dc[pc[j]] - dc[pc[j - 1]]);
+            tb[static_cast<size_t>(c) * (num_taps + 1) + j] = int2{(o >> 4) * tt::rw::kBlockBytes + (o & 15) * 8, gap};
+        }
     }
     auto bail = [&](tt_status s) {
         free_all(h);
@@ -321,14 +408,18 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
         return s;
     };
     cudaError_t e;
-    const size_t ring_b = static_cast<size_t>(num_ue) * snapshot_capacity * num_taps * sizeof(float4);
+    // + one float4: the kernels prefetch one tap ahead
+    const size_t ring_b = (static_cast<size_t>(num_ue) * snapshot_capacity * num_taps + 1) * sizeof(float4);
+    const size_t tb_b = tb.size() * sizeof(int2);
     const size_t hist_b = 2 * static_cast<size_t>(num_ue) * h->H * sizeof(float2);
     const size_t pm_b = pm.size() * sizeof(int32_t), xo_b = xo.size() * sizeof(int32_t);
     if ((e = cudaMalloc(&h->ring, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(snapshot ring)"));
     if (hist_b && (e = cudaMalloc(&h->hist, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(history)"));
     if ((e = cudaMalloc(&h->perm, pm_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
     if ((e = cudaMalloc(&h->xoff, xo_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(xoff)"));
-    h->dev_bytes = ring_b + hist_b + pm_b + xo_b;
+    if ((e = cudaMalloc(&h->tab, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(tab)"));
+    h->dev_bytes = ring_b + hist_b + pm_b + xo_b + tb_b;
+    if ((e = cudaMemcpy(h->tab, tb.data(), tb_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy tab"));
     if ((e = cudaMemcpy(h->perm, pm.data(), pm_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
     if ((e = cudaMemcpy(h->xoff, xo.data(), xo_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy xoff"));
     if (hist_b && (e = cudaMemset(h->hist, 0, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "zero history"));
@@ -493,7 +584,8 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2) +
                                               h->load_stage_elems * sizeof(float2));
     info->outputs_per_thread = h->plan.R;
-    info->launches_per_apply = h->plan.R != 0 ? 1 : (h->H > 0 ? 2 : 1);
+    info->launches_per_apply = h->plan.R != 0 ? 1 : 2;
+    info->kernel = h->plan.rw ? TT_KERNEL_RW : (h->plan.R != 0 ? TT_KERNEL_TILED : TT_KERNEL_GENERIC);
     return TT_OK;
 }
 

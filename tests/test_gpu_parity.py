@@ -159,3 +159,27 @@ def test_error_codes(cuda_device):
         ch.apply(x[:, :1], noise_sigma=-1.0)
     assert ch.t == 47  # failed calls do not advance the stream
     ch.close()
+
+
+@pytest.mark.parametrize("name,kw,calls", [
+    ("c4", dict(ues=2, n_per_call=20_000, calls=1), [20_000]),
+    ("c4", dict(ues=2, n_per_call=20_000, calls=1), [1, 15, 16, 17, 4_095, 4_097, 11_759]),  # 16-misaligned starts
+    ("c3", dict(ues=3, n_per_call=9_001, calls=1), [9_001]),
+    ("c5-L256", dict(ues=2, n_per_call=9_000), [3_000, 6_000]),
+    ("c5-L1", dict(ues=3, n_per_call=5_003), [5_003]),
+    ("c1", dict(n_per_call=7_777), [7_777]),
+])
+def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
+    """The register-window kernel (default for S % 16 == 0), the tiled kernel and the
+    generic kernel run the same per-output operation sequence: outputs are equal bit for
+    bit, for any call split (history carried across 16-misaligned call starts)."""
+    w = ttsynth.get(name).scaled(**kw)
+    run = Run(w, seed=21)
+    outs = {}
+    for k in ("rw", "tiled", "generic"):
+        monkeypatch.setenv("TT_KERNEL", k)
+        outs[k] = run.gpu(cuda_device, calls=calls)
+    monkeypatch.delenv("TT_KERNEL")
+    assert np.array_equal(outs["rw"], outs["tiled"])
+    assert np.array_equal(outs["rw"], outs["generic"])
+    compare(outs["rw"], run.oracle(), name)

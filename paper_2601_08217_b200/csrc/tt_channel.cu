@@ -52,24 +52,32 @@ struct DeviceGuard {
     }
 };
 
-// Launch plan of the tiled kernel for one handle.
-struct Plan {
-    bool rw = false;     // register-window kernel (tt_conv_rw.cuh)
-    int rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
-    int R = 0;           // outputs per consumer thread (0 = generic kernel)
-    int stages = 0;      // shared-memory pipeline depth
+// Launch plan of one handle. kind: TT_KERNEL_GENERIC / TILED / RW. The tiled kernel has
+// one plan per noise flag (they may differ in R if the variants' budgets ever differ).
+struct TiledPlan {
+    int R = 0;           // outputs per consumer thread (0: does not fit -> generic kernel)
     size_t smem = 0;     // dynamic shared memory bytes
-    int nk_max = 0;
+    int nk_max = 0;      // gain rows staged per tile
+};
+struct Plan {
+    int kind = TT_KERNEL_GENERIC;
+    TiledPlan tiled[2];  // [noise]
+    int stages = 2;      // tiled: shared-memory pipeline depth
+    // register-window kernel (opt-in: TT_KERNEL=rw)
+    int rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
+    size_t rw_smem = 0;
 };
 
-constexpr size_t kSmemBudget = 220 * 1024;  // one CTA per SM (227 KB max per CTA)
+constexpr size_t kSmemBudget = 227 * 1024;  // one CTA per SM
 
 // must match tt_conv_kernel's layout: 128 B of barriers + `stages` x [win | coef | xo]
-size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, int* nk_out) {
+// (+ two T-sample noise tiles for the noise variant)
+size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, bool noise, int* nk_out) {
     const int T = tt::kConsumerWarps * 32 * R;
     const int nk = (T - 1) / S + 2;  // worst-case intervals touched by a tile
     *nk_out = nk;
     const size_t st = (static_cast<size_t>(H) + T) * 8 + static_cast<size_t>(nk) * L * 16 + static_cast<size_t>(L4) * 4;
+    (void)noise;  // the noise variant needs no extra shared memory (fused epilogue)
     return 128 + static_cast<size_t>(stages) * st;
 }
 
@@ -93,7 +101,6 @@ struct tt_channel_s {
     size_t load_stage_elems = 0;
     size_t dev_bytes = 0;
     Plan plan;
-    int occ[2] = {0, 0};  // resident CTAs per SM (no noise, noise)
     // host-buffer path
     float2* stage = nullptr;  // 3 x (in + out) chunk buffers
     size_t stage_elems = 0;   // float2 per in (or out) chunk buffer
@@ -104,22 +111,50 @@ struct tt_channel_s {
 namespace {
 
 template <int R, bool NOISE>
-cudaError_t prepare_kernel(size_t smem, int* occ) {
-    auto k = tt::tt_conv_kernel<R, NOISE>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, tt::kThreads, smem);
+cudaError_t prepare_kernel(size_t smem) {
+    return cudaFuncSetAttribute(tt::tt_conv_kernel<R, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem));
+}
+
+template <bool NOISE>
+cudaError_t prepare_tiled(tt_channel_s* h) {
+    TiledPlan& tp = h->plan.tiled[NOISE ? 1 : 0];
+    // candidates that fit; prefer the largest R whose warp span 32R fits in one snapshot
+    // interval (then the gain read is one broadcast per tap), else the largest that fits
+    const int Rs[3] = {8, 4, 2};
+    const bool pow2 = (h->S & (h->S - 1)) == 0;
+    int pick = -1;
+    for (int pass = 0; pass < 2 && pick < 0; ++pass) {
+        for (int i = 0; i < 3; ++i) {
+            int nk = 0;
+            const size_t sm = smem_bytes(Rs[i], h->plan.stages, h->H, h->L, h->L4, h->S, NOISE, &nk);
+            if (sm > kSmemBudget) continue;
+            if (pass == 0 && !(pow2 && 32 * Rs[i] <= h->S)) continue;
+            pick = i;
+            tp.R = Rs[i];
+            tp.smem = sm;
+            tp.nk_max = nk;
+            break;
+        }
+    }
+    switch (tp.R) {
+        case 8: return prepare_kernel<8, NOISE>(tp.smem);
+        case 4: return prepare_kernel<4, NOISE>(tp.smem);
+        case 2: return prepare_kernel<2, NOISE>(tp.smem);
+        default: return cudaSuccess;  // generic kernel
+    }
 }
 
 cudaError_t prepare_plan(tt_channel_s* h) {
     h->plan = Plan{};
-    // TT_KERNEL=rw|tiled|generic restricts the choice (tests compare the paths bit for bit)
+    // TT_KERNEL=rw|tiled|generic selects the kernel (all are bit-identical; default tiled)
     const char* force = getenv("TT_KERNEL");
-    const bool allow_rw = !force || !strcmp(force, "rw");
-    const bool allow_tiled = !force || !strcmp(force, "tiled") || !strcmp(force, "rw");
+    const bool want_rw = force && !strcmp(force, "rw");
+    const bool want_generic = force && !strcmp(force, "generic");
+    if (want_generic) return cudaSuccess;
     // register-window kernel: needs 16-aligned snapshot intervals and two window stages
     // of (Hp + T) / 16 doubled blocks in shared memory
-    if (allow_rw && h->S % 16 == 0) {
+    if (want_rw && h->S % 16 == 0) {
         const int Hp = h->H - 16;
         const int nb = (Hp + tt::rw::T) / 16;
         const size_t wbytes = (static_cast<size_t>(nb) * tt::rw::kBlockBytes + 15) & ~size_t(15);
@@ -128,58 +163,25 @@ cudaError_t prepare_plan(tt_channel_s* h) {
         const size_t tbytes = (static_cast<size_t>(h->L + 1) * 8 + 15) & ~size_t(15);
         const size_t sbytes = wbytes + rows * row_stride + tbytes;
         const size_t sm = 128 + 2 * sbytes;
-        if (sm <= 227 * 1024) {
+        if (sm <= kSmemBudget) {
             h->plan.rw_wbytes = static_cast<int>(wbytes);
             h->plan.rw_rows = static_cast<int>(rows);
             h->plan.rw_row_stride = static_cast<int>(row_stride);
             h->plan.rw_sbytes = static_cast<int>(sbytes);
-            h->plan.rw = true;
-            h->plan.R = tt::rw::R;
-            h->plan.stages = 2;
-            h->plan.smem = sm;
+            h->plan.rw_smem = sm;
+            h->plan.kind = TT_KERNEL_RW;
             cudaError_t e;
             if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(sm))) != cudaSuccess)
                 return e;
-            if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sm))) != cudaSuccess)
-                return e;
-            h->occ[0] = h->occ[1] = 1;
-            return cudaSuccess;
+            return cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sm));
         }
     }
-    // largest R whose two-stage pipeline fits one CTA per SM; else the generic kernel
-    const int Rs[3] = {8, 4, 2};
-    for (int i = 0; allow_tiled && i < 3; ++i) {
-        int nk = 0;
-        const size_t sm = smem_bytes(Rs[i], 2, h->H, h->L, h->L4, h->S, &nk);
-        if (sm <= kSmemBudget) {
-            h->plan.R = Rs[i];
-            h->plan.stages = 2;
-            h->plan.smem = sm;
-            h->plan.nk_max = nk;
-            break;
-        }
-    }
-    if (h->plan.R == 0) return cudaSuccess;
-    int o0 = 0, o1 = 0;
     cudaError_t e;
-    switch (h->plan.R) {
-        case 8:
-            if ((e = prepare_kernel<8, false>(h->plan.smem, &o0)) != cudaSuccess) return e;
-            if ((e = prepare_kernel<8, true>(h->plan.smem, &o1)) != cudaSuccess) return e;
-            break;
-        case 4:
-            if ((e = prepare_kernel<4, false>(h->plan.smem, &o0)) != cudaSuccess) return e;
-            if ((e = prepare_kernel<4, true>(h->plan.smem, &o1)) != cudaSuccess) return e;
-            break;
-        default:
-            if ((e = prepare_kernel<2, false>(h->plan.smem, &o0)) != cudaSuccess) return e;
-            if ((e = prepare_kernel<2, true>(h->plan.smem, &o1)) != cudaSuccess) return e;
-            break;
-    }
-    h->occ[0] = std::max(1, o0);
-    h->occ[1] = std::max(1, o1);
+    if ((e = prepare_tiled<false>(h)) != cudaSuccess) return e;
+    if ((e = prepare_tiled<true>(h)) != cudaSuccess) return e;
+    if (h->plan.tiled[0].R != 0 || h->plan.tiled[1].R != 0) h->plan.kind = TT_KERNEL_TILED;
     return cudaSuccess;
 }
 
@@ -217,7 +219,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     p.t_mod = static_cast<int32_t>(h->t % h->S);
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
-    if (h->plan.rw) {
+    if (h->plan.kind == TT_KERNEL_RW) {
         tt::rw::Params q{};
         q.x = x;
         q.y = y;
@@ -250,26 +252,27 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         q.total_tiles = static_cast<int64_t>(nch) * q.tiles_per_ch;
         const int64_t grid = std::min<int64_t>(q.total_tiles, static_cast<int64_t>(h->num_sms));
         if (noise)
-            tt::rw::tt_conv_rw_kernel<true><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.smem, st>>>(q);
+            tt::rw::tt_conv_rw_kernel<true><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
         else
-            tt::rw::tt_conv_rw_kernel<false><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.smem, st>>>(q);
-    } else if (h->plan.R != 0) {
-        const int T = tt::kConsumerWarps * 32 * h->plan.R;
+            tt::rw::tt_conv_rw_kernel<false><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
+    } else if (h->plan.kind == TT_KERNEL_TILED && h->plan.tiled[noise ? 1 : 0].R != 0) {
+        const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
+        const int T = tt::kConsumerWarps * 32 * tp.R;
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
-        p.nk_max = h->plan.nk_max;
+        p.nk_max = tp.nk_max;
         p.stages = h->plan.stages;
-        const int occ = noise ? h->occ[1] : h->occ[0];
-        const int64_t grid = std::min<int64_t>(p.total_tiles, static_cast<int64_t>(h->num_sms) * occ);
-        const dim3 g(static_cast<unsigned>(grid)), b(tt::kThreads);
-        const size_t sm = h->plan.smem;
-        switch (h->plan.R * 2 + (noise ? 1 : 0)) {
-            case 16: tt::tt_conv_kernel<8, false><<<g, b, sm, st>>>(p); break;
-            case 17: tt::tt_conv_kernel<8, true><<<g, b, sm, st>>>(p); break;
-            case 8: tt::tt_conv_kernel<4, false><<<g, b, sm, st>>>(p); break;
-            case 9: tt::tt_conv_kernel<4, true><<<g, b, sm, st>>>(p); break;
-            case 4: tt::tt_conv_kernel<2, false><<<g, b, sm, st>>>(p); break;
-            default: tt::tt_conv_kernel<2, true><<<g, b, sm, st>>>(p); break;
+        const int64_t grid = std::min<int64_t>(p.total_tiles, static_cast<int64_t>(h->num_sms));
+        const dim3 g(static_cast<unsigned>(grid));
+        const size_t sm = tp.smem;
+        const unsigned b0 = tt::kThreads, b1 = tt::kThreads;
+        switch (tp.R * 2 + (noise ? 1 : 0)) {
+            case 16: tt::tt_conv_kernel<8, false><<<g, b0, sm, st>>>(p); break;
+            case 17: tt::tt_conv_kernel<8, true><<<g, b1, sm, st>>>(p); break;
+            case 8: tt::tt_conv_kernel<4, false><<<g, b0, sm, st>>>(p); break;
+            case 9: tt::tt_conv_kernel<4, true><<<g, b1, sm, st>>>(p); break;
+            case 4: tt::tt_conv_kernel<2, false><<<g, b0, sm, st>>>(p); break;
+            default: tt::tt_conv_kernel<2, true><<<g, b1, sm, st>>>(p); break;
         }
     } else {
         p.tiles_per_ch = 1;
@@ -583,9 +586,10 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->seed = h->seed;
     info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2) +
                                               h->load_stage_elems * sizeof(float2));
-    info->outputs_per_thread = h->plan.R;
-    info->launches_per_apply = h->plan.R != 0 ? 1 : 2;
-    info->kernel = h->plan.rw ? TT_KERNEL_RW : (h->plan.R != 0 ? TT_KERNEL_TILED : TT_KERNEL_GENERIC);
+    info->kernel = h->plan.kind;
+    info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? tt::rw::R
+                               : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R : 0;
+    info->launches_per_apply = h->plan.kind == TT_KERNEL_GENERIC ? 2 : 1;
     return TT_OK;
 }
 

@@ -56,13 +56,13 @@ struct DeviceGuard {
 // one plan per noise flag (they may differ in R if the variants' budgets ever differ).
 struct TiledPlan {
     int R = 0;           // outputs per consumer thread (0: does not fit -> generic kernel)
+    int stages = 2;      // shared-memory pipeline depth (2..4)
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;      // gain rows staged per tile
 };
 struct Plan {
     int kind = TT_KERNEL_GENERIC;
     TiledPlan tiled[2];  // [noise]
-    int stages = 2;      // tiled: shared-memory pipeline depth
     // register-window kernel (opt-in: TT_KERNEL=rw)
     int rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
     size_t rw_smem = 0;
@@ -119,20 +119,27 @@ cudaError_t prepare_kernel(size_t smem) {
 template <bool NOISE>
 cudaError_t prepare_tiled(tt_channel_s* h) {
     TiledPlan& tp = h->plan.tiled[NOISE ? 1 : 0];
-    // candidates that fit; prefer the largest R whose warp span 32R fits in one snapshot
-    // interval (then the gain read is one broadcast per tap), else the largest that fits
+    // deepest pipeline (<= 4 stages) that fits: streaming configs with short filters are
+    // bound by HBM latency x bytes in flight, so they want more tiles in flight
+    const char* fs = getenv("TT_STAGES");
+    const int max_stages = fs ? std::max(2, std::min(tt::kMaxStages, atoi(fs))) : tt::kMaxStages;
+    // the largest R that fits; with a power-of-two S >= 32 a warp's rows read one
+    // broadcast gain row per snapshot interval they cover (tt_conv.cuh taps_grouped)
     const int Rs[3] = {8, 4, 2};
-    const bool pow2 = (h->S & (h->S - 1)) == 0;
+    const bool pow2 = (h->S & (h->S - 1)) == 0 && h->S >= 32;
     int pick = -1;
     for (int pass = 0; pass < 2 && pick < 0; ++pass) {
         for (int i = 0; i < 3; ++i) {
             int nk = 0;
-            const size_t sm = smem_bytes(Rs[i], h->plan.stages, h->H, h->L, h->L4, h->S, NOISE, &nk);
-            if (sm > kSmemBudget) continue;
-            if (pass == 0 && !(pow2 && 32 * Rs[i] <= h->S)) continue;
+            if (smem_bytes(Rs[i], 2, h->H, h->L, h->L4, h->S, NOISE, &nk) > kSmemBudget) continue;
+            if (pass == 0 && !pow2) continue;
+            int stages = max_stages;
+            while (stages > 2 && smem_bytes(Rs[i], stages, h->H, h->L, h->L4, h->S, NOISE, &nk) > kSmemBudget)
+                --stages;
             pick = i;
             tp.R = Rs[i];
-            tp.smem = sm;
+            tp.stages = stages;
+            tp.smem = smem_bytes(Rs[i], stages, h->H, h->L, h->L4, h->S, NOISE, &nk);
             tp.nk_max = nk;
             break;
         }
@@ -261,7 +268,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
         p.nk_max = tp.nk_max;
-        p.stages = h->plan.stages;
+        p.stages = tp.stages;
         const int64_t grid = std::min<int64_t>(p.total_tiles, static_cast<int64_t>(h->num_sms));
         const dim3 g(static_cast<unsigned>(grid));
         const size_t sm = tp.smem;

@@ -245,6 +245,40 @@ __device__ __forceinline__ void mac_tap(const float4 q, const float2* __restrict
     }
 }
 
+// One tap when the warp's R rows (32 outputs each) fall into NG consecutive snapshot
+// intervals of R/NG rows each (rows aligned to interval starts): NG broadcast gain
+// reads per tap instead of one per row.
+template <int R, int NG>
+__device__ __forceinline__ void mac_tap_grouped(const float4* __restrict__ cf, int32_t L, int32_t j,
+                                                const float2* __restrict__ xp, const float (&alpha)[R],
+                                                float2 (&A)[R], float2 (&B)[R]) {
+    constexpr int RPG = R / NG;
+    float4 q[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) q[g] = cf[g * L + j];
+    float2 xv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+    float2 h[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        h[r] = __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q[r / RPG].z, q[r / RPG].w),
+                          make_float2(q[r / RPG].x, q[r / RPG].y));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        A[r] = __ffma2_rn(make_float2(h[r].x, h[r].x), xv[r], A[r]);
+        B[r] = __ffma2_rn(make_float2(h[r].y, h[r].y), xv[r], B[r]);
+    }
+}
+
+template <int R, int NG>
+__device__ __forceinline__ void taps_grouped(const ConvParams& p, const float4* cf, const int32_t* xo,
+                                             const float2* xb, const float (&alpha)[R], float2 (&A)[R],
+                                             float2 (&B)[R]) {
+#pragma unroll 2
+    for (int32_t j = 0; j < p.L; ++j) mac_tap_grouped<R, NG>(cf, p.L, j, xb + xo[j], alpha, A, B);
+}
+
 // Consumer warp: the 32R outputs of warp `cw` in tile `ti`.
 template <int R, bool NOISE>
 __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
@@ -291,6 +325,14 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
                 mac_tap<R>(q3, xb + o.w, alpha, A, B);
             }
             for (; j < p.L; ++j) mac_tap<R>(cf[j], xb + st.xo[j], alpha, A, B);
+        } else if ((R & (R - 1)) == 0 && p.s_shift >= 5 && (32 * R) % p.S == 0 && (wj0 & (p.S - 1)) == 0) {
+            // the warp starts on an interval boundary and spans NG = 32R / S whole intervals
+            const float4* cf = st.coef + static_cast<int64_t>(kw0) * p.L;
+            switch ((32 * R) >> p.s_shift) {
+                case 2: taps_grouped<R, (R >= 2 ? 2 : 1)>(p, cf, st.xo, xb, alpha, A, B); break;
+                case 4: taps_grouped<R, (R >= 4 ? 4 : 1)>(p, cf, st.xo, xb, alpha, A, B); break;
+                default: taps_grouped<R, R>(p, cf, st.xo, xb, alpha, A, B); break;
+            }
         } else {
             for (int32_t j = 0; j < p.L; ++j) {
                 const float2* xp = xb + st.xo[j];

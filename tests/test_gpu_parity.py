@@ -168,6 +168,10 @@ def test_error_codes(cuda_device):
     ("c5-L256", dict(ues=2, n_per_call=9_000), [3_000, 6_000]),
     ("c5-L1", dict(ues=3, n_per_call=5_003), [5_003]),
     ("c1", dict(n_per_call=7_777), [7_777]),
+    ("c4", dict(ues=1, n_per_call=12_288, calls=1, S=128), [12_288]),       # 2 intervals per warp
+    ("c4", dict(ues=1, n_per_call=12_288, calls=1, S=64), [4_096, 8_192]),  # 4 per warp
+    ("c4", dict(ues=1, n_per_call=12_288, calls=1, S=32), [12_288]),        # 8 per warp
+    ("c4", dict(ues=1, n_per_call=12_000, calls=1, S=64), [100, 11_900]),   # warps off interval starts
 ])
 def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     """The register-window kernel (default for S % 16 == 0), the tiled kernel and the

@@ -134,12 +134,39 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
 tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                            tt_stream_t stream);
 
+/* NEXT f4 (§V: each UE "receive[s] and sum[s] signals from all neighboring gNB"
+ * sources): let several channels ("links") read the same input stream. After this call
+ * channel c reads row rows[c] of the `in` buffer of every apply call, which is then
+ * float [num_rows][n_samples][2]; each link keeps its own delay line, gains and noise.
+ * rows = NULL restores the identity (row c, num_rows = C). rows is host memory, copied.
+ * Errors: INVALID_ARG (NULL handle, num_rows <= 0, a row outside [0, num_rows)), CUDA. */
+tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t num_rows);
+
+#define TT_AGG_CHUNK 16 /* channels per partial sum of tt_channel_apply_aggregate */
+
+/* NEXT f1 ("the gNB ... applies convolution independently for each UE ...
+ * and only then aggregates them"; P:330 UE-localised convolution) and f4: apply the
+ * channels and sum them in groups of group_size consecutive channels:
+ *   agg[g][n] = sum_{c = g G}^{(g+1) G - 1} y_c[n]
+ * where y_c is exactly what tt_channel_apply computes for channel c (noise included).
+ * The sum is float32 in a fixed order (so it is bit-identical for any call split):
+ * chunks of TT_AGG_CHUNK consecutive channels are summed in channel order, then the
+ * chunk sums in chunk order. agg: device float [C / G][n_samples][2]. out: device
+ * float [C][n_samples][2] for the per-channel outputs, or NULL (not stored). The input
+ * map (tt_channel_set_input_map) applies. May allocate device scratch for the chunk
+ * sums on first use or growth (like tt_channel_apply_host's staging).
+ * Errors: as tt_channel_apply, plus INVALID_ARG (agg NULL, G <= 0, C % G != 0),
+ * OUT_OF_MEMORY. */
+tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out, float* agg, int32_t group_size,
+                                     int64_t n_samples, float noise_sigma, tt_stream_t stream);
+
 /* Same as tt_channel_apply but `in` and `out` are HOST memory (pinned for full
  * overlap; pageable works but copies synchronously). The library pipelines
  * host->device copies, the kernel and device->host copies over channel chunks on
  * internal streams ordered after / before `stream`; out is complete when `stream`
  * reaches this point. Lazily allocates device staging (3 chunk buffers) on first use
- * or growth. Errors: as tt_channel_apply, plus OUT_OF_MEMORY. */
+ * or growth. Errors: as tt_channel_apply, plus OUT_OF_MEMORY, UNSUPPORTED (an input
+ * map is set: use tt_channel_apply with device buffers). */
 tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                                 tt_stream_t stream);
 

@@ -20,5 +20,6 @@ from .oracle import (  # noqa: F401
     angle_all,
     convolve,
     convolve_points,
+    aggregate,
     OracleError,
 )

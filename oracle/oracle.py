@@ -144,3 +144,20 @@ def convolve_points(delays, S: int, gains, k0: int, x, x0: int, cs, ns, sigma: f
     if r:
         raise OracleError(_ERR.get(r, str(r)))
     return y[:, 0] + 1j * y[:, 1]
+
+
+def aggregate(y, group_size: int) -> np.ndarray:
+    """NEXT f1 / f4: sums of the channel outputs over groups of `group_size` consecutive
+    channels, in double (complex128 [C / group_size][N]).
+
+    P:305 / P:315 (§III-B): the gNB "applies convolution independently for each UE
+    stream, and only then aggregates them"; P:330 (§III-C): with UE-localised
+    convolution the gNB only sums; y_agg[k] = sum_u y_u[k]. P:491-492 (§V): each
+    UE "receive[s] and sum[s] signals from all neighboring gNB" (f4, one group = the
+    links of one UE). The plain definition: an elementwise sum.
+    """
+    y = np.asarray(y, dtype=np.complex128)
+    C, N = y.shape
+    if group_size <= 0 or C % group_size:
+        raise OracleError("group_size must divide the channel count")
+    return y.reshape(C // group_size, group_size, N).sum(axis=1)

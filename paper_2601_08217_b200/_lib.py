@@ -23,6 +23,7 @@ STATUS = {
 }
 TT_MAX_DELAY = 4096
 TT_MAX_TAPS = 4096
+TT_AGG_CHUNK = 16
 
 # functions declared in include/tt_channel.h (tests/test_abi.py checks the header agrees)
 EXPORTS = (
@@ -30,6 +31,8 @@ EXPORTS = (
     "tt_channel_load_snapshots",
     "tt_channel_apply",
     "tt_channel_apply_host",
+    "tt_channel_set_input_map",
+    "tt_channel_apply_aggregate",
     "tt_channel_reset",
     "tt_channel_get_info",
     "tt_channel_destroy",
@@ -87,11 +90,14 @@ def lib() -> ct.CDLL:
             L.tt_channel_load_snapshots.argtypes = [P, P, i64, i64, P]
             L.tt_channel_apply.argtypes = [P, P, P, i64, f32, P]
             L.tt_channel_apply_host.argtypes = [P, P, P, i64, f32, P]
+            L.tt_channel_set_input_map.argtypes = [P, P, i32]
+            L.tt_channel_apply_aggregate.argtypes = [P, P, P, P, i32, i64, f32, P]
             L.tt_channel_reset.argtypes = [P, P]
             L.tt_channel_get_info.argtypes = [P, ct.POINTER(ChannelInfo)]
             L.tt_channel_destroy.argtypes = [P]
             for f in ("tt_channel_create", "tt_channel_load_snapshots", "tt_channel_apply", "tt_channel_apply_host",
-                      "tt_channel_reset", "tt_channel_get_info", "tt_channel_destroy"):
+                      "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset",
+                      "tt_channel_get_info", "tt_channel_destroy"):
                 getattr(L, f).restype = ct.c_int
             L.tt_last_error.argtypes = []
             L.tt_last_error.restype = ct.c_char_p
@@ -127,6 +133,15 @@ def tt_channel_apply(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_si
 def tt_channel_apply_host(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_sigma: float,
                           stream: int) -> None:
     check(lib().tt_channel_apply_host(h, in_ptr, out_ptr, n_samples, noise_sigma, stream))
+
+
+def tt_channel_set_input_map(h: int, rows_ptr: int, num_rows: int) -> None:
+    check(lib().tt_channel_set_input_map(h, rows_ptr, num_rows))
+
+
+def tt_channel_apply_aggregate(h: int, in_ptr: int, out_ptr: int, agg_ptr: int, group_size: int, n_samples: int,
+                               noise_sigma: float, stream: int) -> None:
+    check(lib().tt_channel_apply_aggregate(h, in_ptr, out_ptr, agg_ptr, group_size, n_samples, noise_sigma, stream))
 
 
 def tt_channel_reset(h: int, stream: int) -> None:

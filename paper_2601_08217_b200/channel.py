@@ -89,18 +89,62 @@ class Channel:
               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
         """x: float32 device tensor [C][n][2] (or complex64 [C][n]); returns y alike."""
         xv = torch.view_as_real(x) if x.is_complex() else x
-        if xv.dtype != torch.float32 or xv.dim() != 3 or xv.shape[0] != self.C or xv.shape[2] != 2:
-            raise ValueError(f"x must be float32 [C={self.C}][n][2] or complex64 [C][n]")
+        rows = getattr(self, "in_rows", self.C)
+        if xv.dtype != torch.float32 or xv.dim() != 3 or xv.shape[0] != rows or xv.shape[2] != 2:
+            raise ValueError(f"x must be float32 [{rows}][n][2] or complex64 [{rows}][n]")
         if not xv.is_contiguous():
             raise ValueError("x must be contiguous")
         if out is None:
-            out = torch.empty_like(x)
+            out = torch.empty((self.C,) + tuple(xv.shape[1:]), dtype=torch.float32, device=xv.device)
+            if x.is_complex():
+                out = torch.view_as_complex(out)
         ov = torch.view_as_real(out) if out.is_complex() else out
-        if ov.shape != xv.shape or not ov.is_contiguous() or ov.dtype != torch.float32:
-            raise ValueError("out must match x")
+        if ov.shape != (self.C,) + tuple(xv.shape[1:]) or not ov.is_contiguous() or ov.dtype != torch.float32:
+            raise ValueError(f"out must be contiguous float32 [C={self.C}][n][2]")
         _lib.tt_channel_apply(self.handle, xv.data_ptr(), ov.data_ptr(), int(xv.shape[1]), float(noise_sigma),
                               _stream_ptr(stream))
         return out
+
+    def set_input_map(self, rows, num_rows: Optional[int] = None) -> None:
+        """NEXT f4: channel c reads row rows[c] of the apply input ([num_rows][n][2]);
+        None restores the identity."""
+        if rows is None:
+            _lib.tt_channel_set_input_map(self.handle, None, 0)
+            self.in_rows = self.C
+            return
+        r = np.ascontiguousarray(np.asarray(rows, dtype=np.int32))
+        if r.shape != (self.C,):
+            raise ValueError(f"rows must have one entry per channel ({self.C})")
+        nr = int(r.max()) + 1 if num_rows is None else int(num_rows)
+        _lib.tt_channel_set_input_map(self.handle, r.ctypes.data, nr)
+        self.in_rows = nr
+
+    def apply_aggregate(self, x: torch.Tensor, group_size: int, agg: Optional[torch.Tensor] = None,
+                        out: Optional[torch.Tensor] = None, noise_sigma: float = 0.0,
+                        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """NEXT f1/f4: apply, and sum the outputs of every group of `group_size`
+        consecutive channels: agg [C / group_size][n][2]. `out` ([C][n][2]) optionally
+        receives the per-channel outputs."""
+        xv = torch.view_as_real(x) if x.is_complex() else x
+        rows = getattr(self, "in_rows", self.C)
+        if xv.dtype != torch.float32 or xv.dim() != 3 or xv.shape[0] != rows or xv.shape[2] != 2 or \
+                not xv.is_contiguous():
+            raise ValueError(f"x must be contiguous float32 [{rows}][n][2]")
+        n = int(xv.shape[1])
+        if group_size <= 0 or self.C % group_size:
+            raise ValueError(f"group_size must divide C={self.C}")
+        if agg is None:
+            agg = torch.empty((self.C // group_size, n, 2), dtype=torch.float32, device=xv.device)
+        if agg.shape != (self.C // group_size, n, 2) or not agg.is_contiguous():
+            raise ValueError("agg must be contiguous float32 [C/group_size][n][2]")
+        optr = 0
+        if out is not None:
+            if out.shape != (self.C, n, 2) or not out.is_contiguous() or out.dtype != torch.float32:
+                raise ValueError("out must be contiguous float32 [C][n][2]")
+            optr = out.data_ptr()
+        _lib.tt_channel_apply_aggregate(self.handle, xv.data_ptr(), optr, agg.data_ptr(), int(group_size), n,
+                                        float(noise_sigma), _stream_ptr(stream))
+        return agg
 
     def apply_host(self, x: torch.Tensor, out: torch.Tensor, noise_sigma: float = 0.0,
                    stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:

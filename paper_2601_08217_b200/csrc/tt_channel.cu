@@ -97,6 +97,10 @@ struct tt_channel_s {
     int32_t* perm = nullptr;   // [C][L] original tap index of sorted tap j
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
+    int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
+    int32_t in_rows = 0;        // rows of `in` when in_row is set
+    float2* agg_scratch = nullptr;  // chunk sums / per-channel outputs for tt_channel_apply_aggregate
+    size_t agg_scratch_elems = 0;
     float2* load_stage = nullptr;  // device staging for host-memory snapshot sources
     size_t load_stage_elems = 0;
     size_t dev_bytes = 0;
@@ -176,28 +180,45 @@ cudaError_t prepare_plan(tt_channel_s* h) {
             h->plan.rw_row_stride = static_cast<int>(row_stride);
             h->plan.rw_sbytes = static_cast<int>(sbytes);
             h->plan.rw_smem = sm;
-            h->plan.kind = TT_KERNEL_RW;
             cudaError_t e;
             if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(sm))) != cudaSuccess)
                 return e;
-            return cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(sm));
+            if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sm))) != cudaSuccess)
+                return e;
         }
     }
+    // tiled plans (also behind the rw kernel: aggregation and input maps use them)
     cudaError_t e;
     if ((e = prepare_tiled<false>(h)) != cudaSuccess) return e;
     if ((e = prepare_tiled<true>(h)) != cudaSuccess) return e;
-    if (h->plan.tiled[0].R != 0 || h->plan.tiled[1].R != 0) h->plan.kind = TT_KERNEL_TILED;
+    if (h->plan.rw_smem) h->plan.kind = TT_KERNEL_RW;
+    else if (h->plan.tiled[0].R != 0 || h->plan.tiled[1].R != 0) h->plan.kind = TT_KERNEL_TILED;
     return cudaSuccess;
 }
 
 // Enqueue the convolution of channels [c_lo, c_hi) for this call (no state change).
+// Group-sum request of one launch (tt_channel_apply_aggregate): per-channel outputs go
+// to y (may be nullptr), group sums of G channels to agg, via `scratch` when needed.
+struct AggReq {
+    float2* agg = nullptr;
+    int32_t G = 1;
+    float2* scratch = nullptr;
+};
+
 tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int32_t c_hi, int64_t n, float sigma,
-                 cudaStream_t st) {
+                 cudaStream_t st, const AggReq& ar = AggReq{}) {
     tt::ConvParams p{};
     p.x = x;
     p.y = y;
+    p.in_row = h->in_row;
+    p.group = 1;
+    p.chunk = 1;
+    p.nchunks = 1;
+    const int32_t ngroups = ar.agg ? (c_hi - c_lo) / ar.G : 0;
+    const int32_t KC = ar.agg ? std::min<int32_t>(ar.G, TT_AGG_CHUNK) : 1;
+    const int32_t nchunks = ar.agg ? (ar.G + KC - 1) / KC : 1;
     const size_t hs = static_cast<size_t>(h->C) * h->H;
     p.hist_rd = h->hist + h->p * hs;
     p.hist_wr = h->hist + (1 - h->p) * hs;
@@ -226,7 +247,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     p.t_mod = static_cast<int32_t>(h->t % h->S);
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
-    if (h->plan.kind == TT_KERNEL_RW) {
+    if (h->plan.kind == TT_KERNEL_RW && !ar.agg && !h->in_row) {
         tt::rw::Params q{};
         q.x = x;
         q.y = y;
@@ -262,14 +283,25 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
             tt::rw::tt_conv_rw_kernel<true><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
         else
             tt::rw::tt_conv_rw_kernel<false><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
-    } else if (h->plan.kind == TT_KERNEL_TILED && h->plan.tiled[noise ? 1 : 0].R != 0) {
+    } else if (h->plan.tiled[noise ? 1 : 0].R != 0 && (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row)) {
         const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
         const int T = tt::kConsumerWarps * 32 * tp.R;
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
+        if (ar.agg) {
+            // fused chunk sums: straight into agg when a group is one chunk, else into
+            // scratch partials [groups][nchunks][n] reduced below in chunk order
+            p.group = ar.G;
+            p.chunk = KC;
+            p.nchunks = nchunks;
+            p.agg = nchunks > 1 ? ar.scratch : ar.agg;
+            p.total_super = static_cast<int64_t>(ngroups) * nchunks * p.tiles_per_ch;
+        } else {
+            p.total_super = p.total_tiles;
+        }
         p.nk_max = tp.nk_max;
         p.stages = tp.stages;
-        const int64_t grid = std::min<int64_t>(p.total_tiles, static_cast<int64_t>(h->num_sms));
+        const int64_t grid = std::min<int64_t>(p.total_super, static_cast<int64_t>(h->num_sms));
         const dim3 g(static_cast<unsigned>(grid));
         const size_t sm = tp.smem;
         const unsigned b0 = tt::kThreads, b1 = tt::kThreads;
@@ -281,7 +313,14 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
             case 4: tt::tt_conv_kernel<2, false><<<g, b0, sm, st>>>(p); break;
             default: tt::tt_conv_kernel<2, true><<<g, b1, sm, st>>>(p); break;
         }
+        if (ar.agg && nchunks > 1) {
+            const int64_t tot = static_cast<int64_t>(ngroups) * n;
+            const int64_t gg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);
+            tt::tt_group_sum_kernel<<<static_cast<unsigned>(gg), 256, 0, st>>>(ar.scratch, ar.agg, n, ngroups, ar.G, KC,
+                                                                                nchunks, 1);
+        }
     } else {
+        if (ar.agg && !y) p.y = y = ar.scratch;  // per-channel outputs are needed for the sums
         p.tiles_per_ch = 1;
         p.total_tiles = nch;
         const int64_t N = static_cast<int64_t>(nch) * n;
@@ -294,6 +333,12 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
             const int64_t tot = static_cast<int64_t>(nch) * h->H;
             const int64_t hg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);
             tt::tt_history_kernel<<<static_cast<unsigned>(hg), 256, 0, st>>>(p, nch);
+        }
+        if (ar.agg) {
+            const int64_t tot = static_cast<int64_t>(ngroups) * n;
+            const int64_t gg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);
+            tt::tt_group_sum_kernel<<<static_cast<unsigned>(gg), 256, 0, st>>>(y, ar.agg, n, ngroups, ar.G, KC,
+                                                                                nchunks, 0);
         }
     }
     cudaError_t e = cudaGetLastError();
@@ -322,6 +367,8 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->perm);
     cudaFree(h->xoff);
     cudaFree(h->tab);
+    cudaFree(h->in_row);
+    cudaFree(h->agg_scratch);
     cudaFree(h->load_stage);
     cudaFree(h->stage);
     for (int i = 0; i < 3; ++i) {
@@ -506,6 +553,7 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
                                 tt_stream_t stream) {
     tt_status s = check_apply(h, in, out, n_samples, noise_sigma);
     if (s != TT_OK) return s;
+    if (h->in_row) return fail(TT_ERR_UNSUPPORTED, "apply_host with an input map: use tt_channel_apply");
     DeviceGuard dg(h->dev);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // chunk of channels per pipeline stage: ~64 MiB of input, at least one channel
@@ -565,6 +613,67 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
     return TT_OK;
 }
 
+tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t num_rows) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    DeviceGuard dg(h->dev);
+    if (!rows) {
+        if (h->in_row) {
+            TT_CUDA(cudaDeviceSynchronize(), "input map drain");
+            cudaFree(h->in_row);
+        }
+        h->in_row = nullptr;
+        h->in_rows = 0;
+        return TT_OK;
+    }
+    if (num_rows <= 0) return fail(TT_ERR_INVALID_ARG, "num_rows must be > 0");
+    for (int32_t c = 0; c < h->C; ++c)
+        if (rows[c] < 0 || rows[c] >= num_rows)
+            return fail(TT_ERR_INVALID_ARG, "rows[%d] = %d outside [0, %d)", c, rows[c], num_rows);
+    if (!h->in_row) TT_CUDA(cudaMalloc(&h->in_row, static_cast<size_t>(h->C) * sizeof(int32_t)), "cudaMalloc(input map)");
+    else TT_CUDA(cudaDeviceSynchronize(), "input map drain");
+    TT_CUDA(cudaMemcpy(h->in_row, rows, static_cast<size_t>(h->C) * sizeof(int32_t), cudaMemcpyHostToDevice),
+            "copy input map");
+    h->in_rows = num_rows;
+    return TT_OK;
+}
+
+tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out, float* agg, int32_t group_size,
+                                     int64_t n_samples, float noise_sigma, tt_stream_t stream) {
+    tt_status s = check_apply(h, in, agg, n_samples, noise_sigma);
+    if (s != TT_OK) return s;
+    if (group_size <= 0 || h->C % group_size != 0)
+        return fail(TT_ERR_INVALID_ARG, "group_size %d must divide the %d channels", group_size, h->C);
+    if (out == in) return fail(TT_ERR_INVALID_ARG, "in and out must not overlap");
+    DeviceGuard dg(h->dev);
+    AggReq ar;
+    ar.agg = reinterpret_cast<float2*>(agg);
+    ar.G = group_size;
+    const int32_t KC = std::min<int32_t>(group_size, TT_AGG_CHUNK);
+    const int32_t nchunks = (group_size + KC - 1) / KC;
+    const bool tiled = h->plan.tiled[noise_sigma > 0.0f ? 1 : 0].R != 0;
+    // scratch: chunk sums (tiled, > 1 chunk) or per-channel outputs (generic, out == NULL)
+    size_t need = 0;
+    if (tiled && nchunks > 1) need = static_cast<size_t>(h->C / group_size) * nchunks * n_samples;
+    if (!tiled && !out) need = static_cast<size_t>(h->C) * n_samples;
+    if (need > h->agg_scratch_elems) {
+        if (h->agg_scratch) {
+            TT_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "scratch drain");
+            cudaFree(h->agg_scratch);
+            h->agg_scratch = nullptr;
+            h->agg_scratch_elems = 0;
+        }
+        TT_CUDA(cudaMalloc(&h->agg_scratch, need * sizeof(float2)), "cudaMalloc(aggregate scratch)");
+        h->agg_scratch_elems = need;
+    }
+    ar.scratch = h->agg_scratch;
+    s = launch(h, reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), 0, h->C, n_samples,
+               noise_sigma, static_cast<cudaStream_t>(stream), ar);
+    if (s != TT_OK) return s;
+    h->t += n_samples;
+    if (h->H > 0) h->p ^= 1;
+    return TT_OK;
+}
+
 tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream) {
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
     DeviceGuard dg(h->dev);
@@ -592,7 +701,8 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->channel_offset = h->chan_off;
     info->seed = h->seed;
     info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2) +
-                                              h->load_stage_elems * sizeof(float2));
+                                              h->load_stage_elems * sizeof(float2) +
+                                              h->agg_scratch_elems * sizeof(float2));
     info->kernel = h->plan.kind;
     info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? tt::rw::R
                                : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R : 0;

@@ -43,8 +43,14 @@ constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
 constexpr int kMaxStages = 4;
 
 struct ConvParams {
-    const float2* x;        // [C_launch][n]: row 0 = channel c_lo
-    float2* y;              // [C_launch][n]
+    const float2* x;        // [rows][n]: row of channel c = in_row ? in_row[c] : c - c_lo
+    float2* y;              // [C_launch][n] per-channel outputs, or nullptr (aggregate only)
+    const int32_t* in_row;  // [C] input row per channel (NEXT f4: links share a gNB stream), or nullptr
+    float2* agg;            // group sums [groups][n] (nchunks == 1) or partials [groups][nchunks][n]; or nullptr
+    int32_t group;          // G channels summed per group (1 = no aggregation)
+    int32_t chunk;          // KC channels per chunk (partial sum in one CTA, in channel order)
+    int32_t nchunks;        // ceil(G / KC)
+    int64_t total_super;    // groups * nchunks * tiles_per_ch work items
     const float2* hist_rd;  // [C][H]  last H samples of the stream so far
     float2* hist_wr;        // [C][H]  written with the new history
     const float4* ring;     // [C][cap][L] (g_k, g_{k+1} - g_k), taps sorted by delay
@@ -53,7 +59,7 @@ struct ConvParams {
     int64_t t;              // global index of the call's first sample
     int64_t cap;            // ring slots per channel
     int64_t chan_offset;    // global id of channel 0 (noise key)
-    int64_t total_tiles;    // (c_hi - c_lo) * tiles_per_ch
+    int64_t total_tiles;    // (c_hi - c_lo) * tiles_per_ch (channel tiles)
     int64_t t_div;          // t / S
     int32_t t_mod;          // t % S
     int32_t c_lo;           // first channel of this launch
@@ -156,14 +162,30 @@ __device__ __forceinline__ uint32_t div_S(const ConvParams& p, uint32_t v) {
     return p.s_shift >= 0 ? (v >> p.s_shift) : v / static_cast<uint32_t>(p.S);
 }
 
+// A work item ("super tile"): tile tl of the KC-channel chunk q of group g. Without
+// aggregation (G = 1) it is exactly one channel tile.
+struct SuperInfo {
+    int32_t g, q, tl;
+    int32_t c_first;  // absolute channel of the chunk's first member
+    int32_t kcount;   // channels in the chunk
+};
+__device__ __forceinline__ SuperInfo super_info(const ConvParams& p, int64_t su) {
+    SuperInfo si;
+    const int64_t rest = su / p.tiles_per_ch;
+    si.tl = static_cast<int32_t>(su - rest * p.tiles_per_ch);
+    si.g = static_cast<int32_t>(rest / p.nchunks);
+    si.q = static_cast<int32_t>(rest - static_cast<int64_t>(si.g) * p.nchunks);
+    si.c_first = p.c_lo + si.g * p.group + si.q * p.chunk;
+    const int32_t left = p.group - si.q * p.chunk;
+    si.kcount = left < p.chunk ? left : p.chunk;
+    return si;
+}
+
 template <int R>
-__device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int64_t w) {
+__device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int32_t c, int32_t tl) {
     constexpr int T = kConsumerWarps * 32 * R;
     TileInfo ti;
-    const uint32_t w32 = static_cast<uint32_t>(w);
-    const uint32_t cl = w32 / static_cast<uint32_t>(p.tiles_per_ch);
-    const uint32_t tl = w32 - cl * static_cast<uint32_t>(p.tiles_per_ch);
-    ti.c = p.c_lo + static_cast<int32_t>(cl);
+    ti.c = c;
     ti.i0 = static_cast<int64_t>(tl) * T;
     const int64_t rem = p.n - ti.i0;
     ti.Tt = rem < T ? static_cast<int32_t>(rem) : T;
@@ -186,9 +208,8 @@ struct Stage {
 // Producer warp: stage tile `w` and arm `full` (plain parts first, then the barrier,
 // then the TMA bodies).
 template <int R>
-__device__ __forceinline__ void produce_tile(const ConvParams& p, int64_t w, const Stage& st, uint64_t* full,
+__device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, uint64_t* full,
                                              int lane) {
-    const TileInfo ti = tile_info<R>(p, w);
     const int32_t H = p.H;
     const int64_t lo = ti.i0 - H;
     const int64_t hi = ti.i0 + ti.Tt;
@@ -198,8 +219,8 @@ __device__ __forceinline__ void produce_tile(const ConvParams& p, int64_t w, con
                                static_cast<uint32_t>(nA) * 8u);
     // B: this call's input, call-local [max(lo, 0), hi)
     const int64_t bl = lo < 0 ? 0 : lo;
-    const Piece bx = make_piece(st.win + (bl - lo), p.x + static_cast<int64_t>(ti.c - p.c_lo) * p.n + bl,
-                                static_cast<uint32_t>(hi - bl) * 8u);
+    const int64_t row = p.in_row ? static_cast<int64_t>(__ldg(p.in_row + ti.c)) : static_cast<int64_t>(ti.c - p.c_lo);
+    const Piece bx = make_piece(st.win + (bl - lo), p.x + row * p.n + bl, static_cast<uint32_t>(hi - bl) * 8u);
     // C, D: coefficient rows kb .. kb + nk - 1, wrapping at the ring's capacity
     const int64_t s0 = ti.kb % p.cap;
     const int32_t r1 = static_cast<int32_t>((p.cap - s0) < ti.nk ? (p.cap - s0) : ti.nk);
@@ -282,7 +303,7 @@ __device__ __forceinline__ void taps_grouped(const ConvParams& p, const float4* 
 // Consumer warp: the 32R outputs of warp `cw` in tile `ti`.
 template <int R, bool NOISE>
 __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
-                                             int lane) {
+                                             int lane, bool first, float2 (&acc)[R]) {
     const int32_t obase = cw * 32 * R + lane;
     if (cw * 32 * R < ti.Tt) {
         // per-output interpolation weight alpha = j / S (a multiply when S is a power of
@@ -386,11 +407,19 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
                 }
             }
         }
-        float2* yc = p.y + static_cast<int64_t>(ti.c - p.c_lo) * p.n + ti.i0;
+        if (p.y) {
+            float2* yc = p.y + static_cast<int64_t>(ti.c - p.c_lo) * p.n + ti.i0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int32_t o = obase + r * 32;
-            if (o < ti.Tt) yc[o] = out[r];
+            for (int r = 0; r < R; ++r) {
+                const int32_t o = obase + r * 32;
+                if (o < ti.Tt) yc[o] = out[r];
+            }
+        }
+        if (p.agg) {
+            // running chunk sum in channel order: acc = y_first, then acc += y_k
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                acc[r] = first ? out[r] : make_float2(__fadd_rn(acc[r].x, out[r].x), __fadd_rn(acc[r].y, out[r].y));
         }
     }
     // the tile that ends the call writes the new delay-line history (ping-pong); the
@@ -433,22 +462,41 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
     if (warp == kConsumerWarps) {
         // producer: run ahead of the consumers by up to `stages` tiles
         int it = 0;
-        for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
-            const int s = it % p.stages;
-            const int k = it / p.stages;
-            if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
-            produce_tile<R>(p, w, stage(s), &full[s], lane);
+        for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
+            const SuperInfo si = super_info(p, su);
+            for (int32_t k = 0; k < si.kcount; ++k, ++it) {
+                const int s = it % p.stages;
+                const int kk = it / p.stages;
+                if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
+                produce_tile<R>(p, tile_info<R>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
+            }
         }
     } else {
+        const int32_t obase = warp * 32 * R + lane;
         int it = 0;
-        for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
-            const int s = it % p.stages;
-            const int k = it / p.stages;
-            mbar_wait(&full[s], k & 1);
-            const TileInfo ti = tile_info<R>(p, w);
-            consume_tile<R, NOISE>(p, ti, stage(s), warp, lane);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+        for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
+            const SuperInfo si = super_info(p, su);
+            float2 acc[R];
+            TileInfo ti;
+            for (int32_t k = 0; k < si.kcount; ++k, ++it) {
+                const int s = it % p.stages;
+                const int kk = it / p.stages;
+                mbar_wait(&full[s], kk & 1);
+                ti = tile_info<R>(p, si.c_first + k, si.tl);
+                consume_tile<R, NOISE>(p, ti, stage(s), warp, lane, k == 0, acc);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            if (p.agg && warp * 32 * R < ti.Tt) {
+                // the chunk's sum: straight into the group row, or into its partial row
+                float2* dst = p.agg + (static_cast<int64_t>(si.g) * (p.nchunks > 1 ? p.nchunks : 1) +
+                                       (p.nchunks > 1 ? si.q : 0)) * p.n + ti.i0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * 32;
+                    if (o < ti.Tt) dst[o] = acc[r];
+                }
+            }
         }
     }
 }
@@ -470,7 +518,7 @@ __global__ void __launch_bounds__(256) tt_conv_generic_kernel(const ConvParams p
         const int32_t jj = static_cast<int32_t>(n - k * p.S);
         const float alpha = __fdiv_rn(__uint2float_rn(static_cast<uint32_t>(jj)), __int2float_rn(p.S));
         const float4* cr = p.ring + (static_cast<int64_t>(c) * p.cap + (k % p.cap)) * p.L;
-        const float2* xc = p.x + cl * p.n;
+        const float2* xc = p.x + (p.in_row ? static_cast<int64_t>(__ldg(p.in_row + c)) : cl) * p.n;
         const float2* hc = p.hist_rd + static_cast<int64_t>(c) * p.H;
         const int32_t* xo = p.xoff + static_cast<int64_t>(c) * p.L4;
         float2 A = make_float2(0.f, 0.f), Bv = make_float2(0.f, 0.f);
@@ -505,8 +553,40 @@ __global__ void tt_history_kernel(const ConvParams p, int32_t nch) {
         const int32_t i = static_cast<int32_t>(e - cl * p.H);
         const int32_t c = p.c_lo + static_cast<int32_t>(cl);
         const int64_t m = p.n - p.H + i;  // call-local index of the sample
+        const int64_t row = p.in_row ? static_cast<int64_t>(__ldg(p.in_row + c)) : cl;
         p.hist_wr[static_cast<int64_t>(c) * p.H + i] =
-            m >= 0 ? p.x[cl * p.n + m] : p.hist_rd[static_cast<int64_t>(c) * p.H + (p.H + m)];
+            m >= 0 ? p.x[row * p.n + m] : p.hist_rd[static_cast<int64_t>(c) * p.H + (p.H + m)];
+    }
+}
+
+// Group sums (NEXT f1 UL aggregation, f4 multi-gNB):
+//   agg[g][i] = sum_q P_q[i],  P_q = y_{c_q} + y_{c_q + 1} + ... (chunk q of KC channels)
+// each sum taken left to right in float32 — the order the tiled kernel's fused chunk
+// sums use, so both paths give identical bits. from_partials: src holds the chunk sums
+// P [groups][nchunks][n] (tiled kernel); else src holds per-channel outputs [C][n].
+__global__ void tt_group_sum_kernel(const float2* __restrict__ src, float2* __restrict__ agg, int64_t n,
+                                    int32_t groups, int32_t G, int32_t KC, int32_t nchunks, int32_t from_partials) {
+    const int64_t tot = static_cast<int64_t>(groups) * n;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t g = e / n, i = e - g * n;
+        float2 s = make_float2(0.f, 0.f);
+        for (int32_t q = 0; q < nchunks; ++q) {
+            float2 pq;
+            if (from_partials) {
+                pq = __ldg(src + (g * nchunks + q) * n + i);
+            } else {
+                const int64_t c0 = g * G + static_cast<int64_t>(q) * KC;
+                const int32_t kc = (G - q * KC) < KC ? (G - q * KC) : KC;
+                pq = __ldg(src + c0 * n + i);
+                for (int32_t k = 1; k < kc; ++k) {
+                    const float2 v = __ldg(src + (c0 + k) * n + i);
+                    pq = make_float2(__fadd_rn(pq.x, v.x), __fadd_rn(pq.y, v.y));
+                }
+            }
+            s = q == 0 ? pq : make_float2(__fadd_rn(s.x, pq.x), __fadd_rn(s.y, pq.y));
+        }
+        agg[e] = s;
     }
 }
 

@@ -63,6 +63,16 @@ def sum_over_ranks(value: float, device=None, pg=None) -> float:
     return _reduce(value, "SUM", device, pg)
 
 
+def reduce_groups(agg, pg=None):
+    """NEXT f1: when a cell's UEs are sharded over ranks each rank holds the partial
+    group sums of its own UEs (tt_channel_apply_aggregate); the cell's aggregate is
+    their sum over ranks (the path's only data collective: one NCCL all-reduce of
+    groups x n complex samples, ~0.5 MB per cell per c4 slot). In place; returns agg."""
+    if pg is not None:
+        pg.all_reduce(agg, op=pg.ReduceOp.SUM)
+    return agg
+
+
 def barrier(pg=None, device: Optional[object] = None) -> None:
     if pg is not None:
         pg.barrier()

@@ -1,0 +1,126 @@
+"""NEXT rows f1 (UL aggregation at the gNB) and f4 (multi-gNB links) on the GPU,
+through the C ABI: tt_channel_apply_aggregate and tt_channel_set_input_map.
+
+Parity: the group sums match the oracle (double sums of double channel outputs)
+within north_star's tolerances; the fused chunk sums equal, bit for bit, a float32
+left-to-right emulation of the documented order over the same call's per-channel
+outputs; results are bit-identical for any call split and on every kernel path."""
+import numpy as np
+import pytest
+
+import oracle
+import ttsynth
+from harness import Run, compare, to_c
+
+pytestmark = pytest.mark.gpu
+
+CHUNK = 16  # TT_AGG_CHUNK
+
+
+def _chunked_sum_f32(y, G):
+    """The documented order: chunks of CHUNK channels summed left to right in float32,
+    then the chunk sums left to right."""
+    C, N, _ = y.shape
+    out = np.empty((C // G, N, 2), np.float32)
+    for g in range(C // G):
+        s = None
+        for q0 in range(0, G, CHUNK):
+            p = y[g * G + q0].copy()
+            for k in range(1, min(CHUNK, G - q0)):
+                p = (p + y[g * G + q0 + k]).astype(np.float32)
+            s = p if s is None else (s + p).astype(np.float32)
+        out[g] = s
+    return out
+
+
+def _run_aggregate(run, device, G, calls, rows=None, x_rows=None, with_out=True):
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    ch = Channel(run.delays, run.w.S, seed=run.seed, snapshot_capacity=run.K, channel_offset=run.c_lo, device=device)
+    try:
+        ch.load_snapshots(torch.from_numpy(run.gains).to(device), 0)
+        src = run.x if x_rows is None else x_rows
+        if rows is not None:
+            ch.set_input_map(rows, src.shape[0])
+        ys, aggs, pos = [], [], 0
+        for n in calls:
+            xs = torch.from_numpy(np.ascontiguousarray(src[:, pos:pos + n])).to(device)
+            out = torch.empty((run.C, n, 2), dtype=torch.float32, device=device) if with_out else None
+            agg = ch.apply_aggregate(xs, G, out=out, noise_sigma=run.sigma)
+            aggs.append(agg.cpu().numpy())
+            if with_out:
+                ys.append(out.cpu().numpy())
+            pos += n
+        torch.cuda.synchronize()
+    finally:
+        ch.close()
+    return (np.concatenate(ys, axis=1) if with_out else None), np.concatenate(aggs, axis=1)
+
+
+@pytest.mark.parametrize("G", [1, 2, 16, 17, 40])
+@pytest.mark.parametrize("snr", [None, 15.0])
+def test_ul_aggregation_parity_and_order(cuda_device, G, snr):
+    """f1: agg[g] = sum of the group's channel outputs: oracle parity, and the fused
+    chunk sums equal the float32 emulation of the documented order bit for bit."""
+    C = G * (4 if G < 16 else 2)  # groups of G consecutive channels
+    w = ttsynth.get("c3").scaled(ues=C, dirs=1, n_per_call=7_001, calls=1, snr_db=snr)
+    run = Run(w, seed=31)
+    y, agg = _run_aggregate(run, cuda_device, G, [7_001])
+    assert np.array_equal(agg, _chunked_sum_f32(y, G))
+    ref = oracle.aggregate(run.oracle(), G)
+    compare(agg, ref, f"aggregate G={G}")
+
+
+def test_aggregation_streaming_and_kernel_paths_bit_identical(cuda_device, monkeypatch):
+    w = ttsynth.get("c4").scaled(ues=12, dirs=2, n_per_call=9_000, calls=1)
+    run = Run(w, seed=5)
+    _, one = _run_aggregate(run, cuda_device, 24, [9_000], with_out=False)
+    _, split = _run_aggregate(run, cuda_device, 24, [1, 4_095, 17, 4_887], with_out=False)
+    assert np.array_equal(one, split)
+    monkeypatch.setenv("TT_KERNEL", "generic")
+    _, gen = _run_aggregate(run, cuda_device, 24, [9_000], with_out=False)
+    monkeypatch.delenv("TT_KERNEL")
+    assert np.array_equal(one, gen)
+    compare(one, oracle.aggregate(run.oracle(), 24), "c4 UL aggregate")
+
+
+def test_multi_gnb_links(cuda_device):
+    """f4: U UEs x B gNBs links (c = u B + b) reading the B gNB streams
+    through the input map; agg[u] = the UE's received sum over its links."""
+    U, B = 5, 3
+    w = ttsynth.get("c3").scaled(ues=U * B, dirs=1, n_per_call=6_000, calls=1, snr_db=20.0)
+    run = Run(w, seed=77)
+    xg = ttsynth.iq(w, 0, B, 0)  # the B gNB transmit streams
+    rows = np.tile(np.arange(B, dtype=np.int32), U)
+    run.x = xg[rows]  # what each link sees, for the oracle
+    y, agg = _run_aggregate(run, cuda_device, B, [2_500, 3_500], rows=rows, x_rows=xg)
+    compare(y, run.oracle(), "links")
+    compare(agg, oracle.aggregate(run.oracle(), B), "UE sums")
+    assert np.array_equal(agg, _chunked_sum_f32(y, B))
+
+
+def test_input_map_plain_apply_and_errors(cuda_device):
+    import torch
+
+    from paper_2601_08217_b200 import Channel, TTError
+
+    w = ttsynth.get("c3").scaled(ues=4, dirs=1, n_per_call=3_000, calls=1)
+    run = Run(w, seed=3)
+    xg = run.x[:2].copy()
+    rows = np.array([1, 0, 1, 1], np.int32)
+    ch = Channel(run.delays, w.S, seed=3, snapshot_capacity=run.K, device=cuda_device)
+    ch.load_snapshots(torch.from_numpy(run.gains).to(cuda_device), 0)
+    with pytest.raises(TTError, match="INVALID_ARG"):
+        ch.set_input_map(np.array([0, 1, 2, 5], np.int32), 3)
+    ch.set_input_map(rows, 2)
+    y = ch.apply(torch.from_numpy(xg).to(cuda_device), noise_sigma=run.sigma).cpu().numpy()
+    xh = torch.zeros((4, 10, 2)).pin_memory()
+    with pytest.raises(TTError, match="UNSUPPORTED"):
+        ch.apply_host(xh, torch.zeros_like(xh).pin_memory())
+    with pytest.raises(ValueError):
+        ch.apply_aggregate(torch.from_numpy(xg).to(cuda_device), 3)
+    ch.close()
+    run.x = xg[rows]
+    compare(y, run.oracle(), "mapped apply")

@@ -102,3 +102,47 @@ def test_ue_block_rule(ues, dirs, world):
     assert blocks == [ttsynth.shard_ues(w, r, world) for r in range(world)]
     with pytest.raises(ValueError):
         shard.ue_block(ues, dirs, world, world)
+
+
+def _agg_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    try:
+        pg = shard.init("gloo")
+        w = ttsynth.get("c4").scaled(ues=5, dirs=1, n_per_call=1_500, calls=1)  # 5 UL channels, one cell
+        c_lo, c_hi = shard.ue_block(w.ues, w.dirs, rank, world)
+        n = w.n_per_call
+        K = (n - 1) // w.S + 2
+        y = oracle.convolve(ttsynth.delays(w, c_lo, c_hi), w.S, ttsynth.snapshots(w, c_lo, c_hi, K), 0,
+                            ttsynth.iq(w, c_lo, c_hi, 0), 0, 0, n, sigma=w.sigma, seed=9, c_offset=c_lo)
+        part = oracle.aggregate(y, c_hi - c_lo)[0]  # this rank's partial cell sum
+        t = torch.from_numpy(np.stack([part.real, part.imag], axis=-1))
+        shard.reduce_groups(t, pg)
+        if rank == 0:
+            q.put(("ok", t.numpy()))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e)))
+        raise
+
+
+def test_cell_aggregate_reduced_over_ranks():
+    """f1 across ranks: per-rank partial cell sums all-reduced == the single-process
+    cell aggregate (summation order differs -> tolerance)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    status, got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert status == "ok", got
+    w = ttsynth.get("c4").scaled(ues=5, dirs=1, n_per_call=1_500, calls=1)
+    n = w.n_per_call
+    K = (n - 1) // w.S + 2
+    full = oracle.aggregate(oracle.convolve(ttsynth.delays(w), w.S, ttsynth.snapshots(w, 0, w.C, K), 0,
+                                            ttsynth.iq(w, 0, w.C, 0), 0, 0, n, sigma=w.sigma, seed=9), w.C)[0]
+    assert np.allclose(got[:, 0] + 1j * got[:, 1], full, rtol=0, atol=1e-12)

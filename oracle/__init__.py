@@ -21,5 +21,6 @@ from .oracle import (  # noqa: F401
     convolve,
     convolve_points,
     aggregate,
+    select_top_n,
     OracleError,
 )

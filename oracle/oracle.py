@@ -51,6 +51,10 @@ def lib() -> ct.CDLL:
             L.tto_angle_all.argtypes = [P]
             L.tto_convolve.argtypes = [i32, i32, P, i32, P, i64, i64, P, i64, i64, i64, i64, f32, u64, i64, P]
             L.tto_convolve.restype = ct.c_int
+            L.tto_convolve_topn.argtypes = [i32, i32, P, i32, P, i64, i64, P, i64, i64, i64, i64, f32, u64, i64, i32, P]
+            L.tto_convolve_topn.restype = ct.c_int
+            L.tto_select_top_n.argtypes = [i32, P, P, i32, P]
+            L.tto_select_top_n.restype = None
             L.tto_convolve_points.argtypes = [i32, i32, P, i32, P, i64, i64, P, i64, i64, P, P, i64, f32,
                                               u64, i64, P]
             L.tto_convolve_points.restype = ct.c_int
@@ -117,16 +121,17 @@ def _prep(delays, gains, x):
 
 
 def convolve(delays, S: int, gains, k0: int, x, x0: int, n0: int, N: int, sigma: float = 0.0,
-             seed: int = 0, c_offset: int = 0) -> np.ndarray:
+             seed: int = 0, c_offset: int = 0, top_n: int = 0) -> np.ndarray:
     """Outputs y_c[n0 .. n0+N-1] (complex128 [C][N]) of the plain definition.
 
     delays [C][L] int; gains [C][K][L][2] float32 holding snapshots k0..k0+K-1;
     x [C][Nx][2] float32 holding stream samples x0..x0+Nx-1 (samples < 0 are zero).
+    top_n in [1, L): NEXT f2, each interval sums only its top-n taps (select_top_n).
     """
     d, g, xx, C, L = _prep(delays, gains, x)
     y = np.zeros((C, N, 2), dtype=np.float64)
-    r = lib().tto_convolve(C, L, _ptr(d), S, _ptr(g), k0, g.shape[1], _ptr(xx), x0, xx.shape[1], n0, N,
-                           sigma, seed, c_offset, _ptr(y))
+    r = lib().tto_convolve_topn(C, L, _ptr(d), S, _ptr(g), k0, g.shape[1], _ptr(xx), x0, xx.shape[1], n0, N,
+                                sigma, seed, c_offset, int(top_n), _ptr(y))
     if r:
         raise OracleError(_ERR.get(r, str(r)))
     return y[..., 0] + 1j * y[..., 1]
@@ -161,3 +166,13 @@ def aggregate(y, group_size: int) -> np.ndarray:
     if group_size <= 0 or C % group_size:
         raise OracleError("group_size must divide the channel count")
     return y.reshape(C // group_size, group_size, N).sum(axis=1)
+
+
+def select_top_n(delays_row, g_row, n: int) -> np.ndarray:
+    """NEXT f2 selection for one snapshot row: bool [L], the n taps of largest float32
+    |g|^2 (ties: smaller delay, then smaller index). See tt_oracle.c tto_select_top_n."""
+    d = np.ascontiguousarray(delays_row, dtype=np.int32)
+    g = np.ascontiguousarray(g_row, dtype=np.float32)
+    sel = np.zeros(len(d), dtype=np.uint8)
+    lib().tto_select_top_n(len(d), _ptr(d), _ptr(g), int(n), _ptr(sel))
+    return sel.astype(bool)

@@ -170,19 +170,51 @@ void tto_noise_block(uint64_t seed, int64_t c_global, int64_t n0, int64_t N, flo
 }
 
 /* ---------------------------------------------------------------------------
+ * NEXT f2: sparse top-n taps (§III-C "convolution is performed only with the
+ * top-n dominant taps at each time step"). DESIGN.md reading R20: the time
+ * step is the snapshot interval; interval k uses the n taps of largest |g_{l,k}| (its
+ * opening snapshot); "dominant" is compared on m_l = |g_{l,k}|^2 computed in float32
+ * as fl(fl(re*re) + fl(im*im)) (the decision is taken in the kernel's precision); ties
+ * go to the smaller delay, then the smaller tap index ("ties broken toward
+ * smaller bin index"). sel[l] = 1 iff fewer than n taps precede l in that order.
+ * ------------------------------------------------------------------------- */
+void tto_select_top_n(int32_t L, const int32_t* d, const float* g_row /* [L][2] */, int32_t n,
+                      uint8_t* sel /* [L] */) {
+    for (int32_t l = 0; l < L; ++l) {
+        float ml = g_row[2 * l] * g_row[2 * l] + g_row[2 * l + 1] * g_row[2 * l + 1];
+        int32_t rank = 0;
+        for (int32_t i = 0; i < L; ++i) {
+            float mi = g_row[2 * i] * g_row[2 * i] + g_row[2 * i + 1] * g_row[2 * i + 1];
+            int before = mi > ml || (mi == ml && (d[i] < d[l] || (d[i] == d[l] && i < l)));
+            rank += before;
+        }
+        sel[l] = (uint8_t)(rank < n);
+    }
+}
+
+/* ---------------------------------------------------------------------------
  * The convolution (NS formula). One output sample.
+ * top_n in [1, L) restricts the sum to the taps tto_select_top_n picks for the
+ * output's interval (f2); top_n <= 0 or >= L is the dense sum.
  * ------------------------------------------------------------------------- */
 static int one_output(int32_t L, const int32_t* d /* [L] */, int32_t S,
                       const float* g /* [K][L][2] */, int64_t k0, int64_t K,
                       const float* x /* [Nx][2] */, int64_t x0, int64_t Nx,
-                      int64_t n, float sc, uint64_t seed, int64_t c_global, double out[2]) {
+                      int64_t n, float sc, uint64_t seed, int64_t c_global, int32_t top_n, double out[2]) {
     int64_t k = n / S;                     /* n >= 0: floor */
     int64_t j = n - k * S;
     double alpha = (double)j / (double)S;
     int64_t i0 = k - k0;
     if (i0 < 0 || i0 + 1 >= K) return TTO_ESNAPMISSING;
+    uint8_t sel_buf[4096];
+    const int sparse = top_n > 0 && top_n < L;
+    if (sparse) {
+        if (L > 4096) return TTO_EINVAL;
+        tto_select_top_n(L, d, g + i0 * L * 2, top_n, sel_buf);
+    }
     double yr = 0.0, yi = 0.0;
     for (int32_t l = 0; l < L; ++l) {
+        if (sparse && !sel_buf[l]) continue;
         double g0r = g[(i0 * L + l) * 2], g0i = g[(i0 * L + l) * 2 + 1];
         double g1r = g[((i0 + 1) * L + l) * 2], g1i = g[((i0 + 1) * L + l) * 2 + 1];
         double hr = g0r + alpha * (g1r - g0r);
@@ -218,9 +250,9 @@ static int check_common(int32_t C, int32_t L, const int32_t* delays, int32_t S, 
 /* Block form: outputs n0 .. n0+N-1 of every channel.
  *   delays [C][L]; gains [C][K][L][2] = snapshots k0 .. k0+K-1;
  *   x [C][Nx][2] = stream samples x0 .. x0+Nx-1; y [C][N][2] (double). */
-int tto_convolve(int32_t C, int32_t L, const int32_t* delays, int32_t S, const float* gains,
-                 int64_t k0, int64_t K, const float* x, int64_t x0, int64_t Nx, int64_t n0,
-                 int64_t N, float sigma, uint64_t seed, int64_t c_offset, double* y) {
+int tto_convolve_topn(int32_t C, int32_t L, const int32_t* delays, int32_t S, const float* gains,
+                      int64_t k0, int64_t K, const float* x, int64_t x0, int64_t Nx, int64_t n0,
+                      int64_t N, float sigma, uint64_t seed, int64_t c_offset, int32_t top_n, double* y) {
     int st = check_common(C, L, delays, S, sigma);
     if (st) return st;
     if (n0 < 0 || N < 0 || K < 0 || Nx < 0 || x0 < 0) return TTO_EINVAL;
@@ -233,7 +265,7 @@ int tto_convolve(int32_t C, int32_t L, const int32_t* delays, int32_t S, const f
         for (int64_t b = 0; b < nb; ++b) {
             for (int64_t i = b * B; i < N && i < (b + 1) * B; ++i) {
                 int r = one_output(L, delays + (int64_t)c * L, S, gains + (int64_t)c * K * L * 2, k0, K,
-                                   x + (int64_t)c * Nx * 2, x0, Nx, n0 + i, sc, seed, c_offset + c,
+                                   x + (int64_t)c * Nx * 2, x0, Nx, n0 + i, sc, seed, c_offset + c, top_n,
                                    y + ((int64_t)c * N + i) * 2);
                 if (r) {
 #pragma omp atomic write
@@ -243,6 +275,12 @@ int tto_convolve(int32_t C, int32_t L, const int32_t* delays, int32_t S, const f
         }
     }
     return err;
+}
+
+int tto_convolve(int32_t C, int32_t L, const int32_t* delays, int32_t S, const float* gains,
+                 int64_t k0, int64_t K, const float* x, int64_t x0, int64_t Nx, int64_t n0,
+                 int64_t N, float sigma, uint64_t seed, int64_t c_offset, double* y) {
+    return tto_convolve_topn(C, L, delays, S, gains, k0, K, x, x0, Nx, n0, N, sigma, seed, c_offset, 0, y);
 }
 
 /* Point form: outputs at (cs[p], ns[p]), p < P; same input layouts; y [P][2]. */
@@ -261,7 +299,7 @@ int tto_convolve_points(int32_t C, int32_t L, const int32_t* delays, int32_t S, 
         if (c < 0 || c >= C || ns[p] < 0) r = TTO_EINVAL;
         else
             r = one_output(L, delays + (int64_t)c * L, S, gains + (int64_t)c * K * L * 2, k0, K,
-                           x + (int64_t)c * Nx * 2, x0, Nx, ns[p], sc, seed, c_offset + c, y + p * 2);
+                           x + (int64_t)c * Nx * 2, x0, Nx, ns[p], sc, seed, c_offset + c, 0, y + p * 2);
         if (r) {
 #pragma omp atomic write
             err = r;

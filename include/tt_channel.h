@@ -80,6 +80,7 @@ typedef struct {
     int32_t outputs_per_thread; /* outputs per thread of the selected kernel (0 = generic kernel) */
     int32_t launches_per_apply; /* kernel launches one tt_channel_apply enqueues */
     int32_t kernel;             /* TT_KERNEL_* the plan selected */
+    int32_t top_n;              /* NEXT f2 taps per interval (0 = dense) */
 } tt_channel_info;
 
 /* kernels a plan can select (all compute the same per-output operation sequence, so
@@ -133,6 +134,16 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
  *   not finite), SNAPSHOT_MISSING, CUDA (launch failure). */
 tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                            tt_stream_t stream);
+
+/* NEXT f2 (§III-C "convolution is performed only with the top-n dominant taps at
+ * each time step"): from now on each snapshot interval k sums only its top_n taps of
+ * largest |g_{l,k}|^2 (float32 fl(re*re) + fl(im*im); ties to the smaller delay, then
+ * the smaller tap index), in ascending-delay order, interpolated as usual (DESIGN.md
+ * R20). top_n = 0 or >= L restores the dense sum (the default). Selection happens when
+ * snapshots are loaded; this call also (re)selects every resident snapshot. Allocates
+ * the compacted ring (C x capacity x top_n x 20 B). Synchronises the device.
+ * Errors: INVALID_ARG (NULL handle, top_n < 0), OUT_OF_MEMORY, CUDA. */
+tt_status tt_channel_set_top_n(tt_channel_t h, int32_t top_n);
 
 /* NEXT f4 (§V: each UE "receive[s] and sum[s] signals from all neighboring gNB"
  * sources): let several channels ("links") read the same input stream. After this call

@@ -10,7 +10,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(PKG, "libtt.so")
+SO = os.environ.get("TT_LIB") or os.path.join(PKG, "libtt.so")  # TT_LIB: A/B experiments only
 
 TT_OK = 0
 STATUS = {
@@ -31,6 +31,7 @@ EXPORTS = (
     "tt_channel_load_snapshots",
     "tt_channel_apply",
     "tt_channel_apply_host",
+    "tt_channel_set_top_n",
     "tt_channel_set_input_map",
     "tt_channel_apply_aggregate",
     "tt_channel_reset",
@@ -66,6 +67,7 @@ class ChannelInfo(ct.Structure):
         ("outputs_per_thread", ct.c_int32),
         ("launches_per_apply", ct.c_int32),
         ("kernel", ct.c_int32),
+        ("top_n", ct.c_int32),
     ]
 
 
@@ -90,13 +92,15 @@ def lib() -> ct.CDLL:
             L.tt_channel_load_snapshots.argtypes = [P, P, i64, i64, P]
             L.tt_channel_apply.argtypes = [P, P, P, i64, f32, P]
             L.tt_channel_apply_host.argtypes = [P, P, P, i64, f32, P]
+            L.tt_channel_set_top_n.argtypes = [P, i32]
             L.tt_channel_set_input_map.argtypes = [P, P, i32]
             L.tt_channel_apply_aggregate.argtypes = [P, P, P, P, i32, i64, f32, P]
             L.tt_channel_reset.argtypes = [P, P]
             L.tt_channel_get_info.argtypes = [P, ct.POINTER(ChannelInfo)]
             L.tt_channel_destroy.argtypes = [P]
             for f in ("tt_channel_create", "tt_channel_load_snapshots", "tt_channel_apply", "tt_channel_apply_host",
-                      "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset",
+                      "tt_channel_set_top_n",
+    "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset",
                       "tt_channel_get_info", "tt_channel_destroy"):
                 getattr(L, f).restype = ct.c_int
             L.tt_last_error.argtypes = []
@@ -133,6 +137,10 @@ def tt_channel_apply(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_si
 def tt_channel_apply_host(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_sigma: float,
                           stream: int) -> None:
     check(lib().tt_channel_apply_host(h, in_ptr, out_ptr, n_samples, noise_sigma, stream))
+
+
+def tt_channel_set_top_n(h: int, top_n: int) -> None:
+    check(lib().tt_channel_set_top_n(h, top_n))
 
 
 def tt_channel_set_input_map(h: int, rows_ptr: int, num_rows: int) -> None:

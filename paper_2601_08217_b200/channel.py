@@ -105,6 +105,10 @@ class Channel:
                               _stream_ptr(stream))
         return out
 
+    def set_top_n(self, top_n: int) -> None:
+        """NEXT f2: sum only the top_n dominant taps per snapshot interval (0 = dense)."""
+        _lib.tt_channel_set_top_n(self.handle, int(top_n))
+
     def set_input_map(self, rows, num_rows: Optional[int] = None) -> None:
         """NEXT f4: channel c reads row rows[c] of the apply input ([num_rows][n][2]);
         None restores the identity."""

@@ -71,12 +71,13 @@ struct Plan {
 constexpr size_t kSmemBudget = 227 * 1024;  // one CTA per SM
 
 // must match tt_conv_kernel's layout: 128 B of barriers + `stages` x [win | coef | xo]
-// (+ two T-sample noise tiles for the noise variant)
-size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, bool noise, int* nk_out) {
+// (L = taps per gain row: top-n when sparse, whose offsets come one row per interval)
+size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, bool noise, bool xo_rows, int* nk_out) {
     const int T = tt::kConsumerWarps * 32 * R;
     const int nk = (T - 1) / S + 2;  // worst-case intervals touched by a tile
     *nk_out = nk;
-    const size_t st = (static_cast<size_t>(H) + T) * 8 + static_cast<size_t>(nk) * L * 16 + static_cast<size_t>(L4) * 4;
+    const size_t st = (static_cast<size_t>(H) + T) * 8 + static_cast<size_t>(nk) * L * 16 +
+                      static_cast<size_t>(xo_rows ? nk : 1) * L4 * 4;
     (void)noise;  // the noise variant needs no extra shared memory (fused epilogue)
     return 128 + static_cast<size_t>(stages) * st;
 }
@@ -98,6 +99,10 @@ struct tt_channel_s {
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
     int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
+    int32_t top_n = 0;          // NEXT f2: taps kept per interval (0 = dense)
+    int32_t n4 = 0;             // sparse offsets row stride (>= top_n + 1, multiple of 4)
+    float4* sring = nullptr;    // [C][cap][top_n] (+1) compacted rows of the selected taps
+    int32_t* soff = nullptr;    // [C][cap][n4] window offsets of the selected taps
     int32_t in_rows = 0;        // rows of `in` when in_row is set
     float2* agg_scratch = nullptr;  // chunk sums / per-channel outputs for tt_channel_apply_aggregate
     size_t agg_scratch_elems = 0;
@@ -116,7 +121,10 @@ namespace {
 
 template <int R, bool NOISE>
 cudaError_t prepare_kernel(size_t smem) {
-    return cudaFuncSetAttribute(tt::tt_conv_kernel<R, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(tt::tt_conv_kernel<R, NOISE, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(tt::tt_conv_kernel<R, NOISE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem));
 }
 
@@ -127,6 +135,8 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     // bound by HBM latency x bytes in flight, so they want more tiles in flight
     const char* fs = getenv("TT_STAGES");
     const int max_stages = fs ? std::max(2, std::min(tt::kMaxStages, atoi(fs))) : tt::kMaxStages;
+    const bool sparse = h->top_n > 0;
+    const int Lr = sparse ? h->top_n : h->L, L4r = sparse ? h->n4 : h->L4;
     // the largest R that fits; with a power-of-two S >= 32 a warp's rows read one
     // broadcast gain row per snapshot interval they cover (tt_conv.cuh taps_grouped)
     const int Rs[3] = {8, 4, 2};
@@ -135,15 +145,15 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     for (int pass = 0; pass < 2 && pick < 0; ++pass) {
         for (int i = 0; i < 3; ++i) {
             int nk = 0;
-            if (smem_bytes(Rs[i], 2, h->H, h->L, h->L4, h->S, NOISE, &nk) > kSmemBudget) continue;
+            if (smem_bytes(Rs[i], 2, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget) continue;
             if (pass == 0 && !pow2) continue;
             int stages = max_stages;
-            while (stages > 2 && smem_bytes(Rs[i], stages, h->H, h->L, h->L4, h->S, NOISE, &nk) > kSmemBudget)
+            while (stages > 2 && smem_bytes(Rs[i], stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget)
                 --stages;
             pick = i;
             tp.R = Rs[i];
             tp.stages = stages;
-            tp.smem = smem_bytes(Rs[i], stages, h->H, h->L, h->L4, h->S, NOISE, &nk);
+            tp.smem = smem_bytes(Rs[i], stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk);
             tp.nk_max = nk;
             break;
         }
@@ -222,15 +232,17 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     const size_t hs = static_cast<size_t>(h->C) * h->H;
     p.hist_rd = h->hist + h->p * hs;
     p.hist_wr = h->hist + (1 - h->p) * hs;
-    p.ring = h->ring;
+    const bool sparse = h->top_n > 0;
+    p.ring = sparse ? h->sring : h->ring;
     p.xoff = h->xoff;
+    p.xoff_rows = sparse ? h->soff : nullptr;
     p.n = n;
     p.t = h->t;
     p.cap = h->cap;
     p.chan_offset = h->chan_off;
     p.c_lo = c_lo;
-    p.L = h->L;
-    p.L4 = h->L4;
+    p.L = sparse ? h->top_n : h->L;
+    p.L4 = sparse ? h->n4 : h->L4;
     p.H = h->H;
     p.S = h->S;
     p.key0 = static_cast<uint32_t>(h->seed);
@@ -247,7 +259,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     p.t_mod = static_cast<int32_t>(h->t % h->S);
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
-    if (h->plan.kind == TT_KERNEL_RW && !ar.agg && !h->in_row) {
+    if (h->plan.kind == TT_KERNEL_RW && !ar.agg && !h->in_row && !sparse) {
         tt::rw::Params q{};
         q.x = x;
         q.y = y;
@@ -283,7 +295,8 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
             tt::rw::tt_conv_rw_kernel<true><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
         else
             tt::rw::tt_conv_rw_kernel<false><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
-    } else if (h->plan.tiled[noise ? 1 : 0].R != 0 && (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row)) {
+    } else if (h->plan.tiled[noise ? 1 : 0].R != 0 &&
+               (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row || sparse)) {
         const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
         const int T = tt::kConsumerWarps * 32 * tp.R;
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
@@ -301,17 +314,27 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         }
         p.nk_max = tp.nk_max;
         p.stages = tp.stages;
+        if (p.total_super >= (int64_t(1) << 31) || p.total_tiles >= (int64_t(1) << 31))
+            return fail(TT_ERR_INVALID_ARG, "call too large: %lld work items", (long long)p.total_super);
         const int64_t grid = std::min<int64_t>(p.total_super, static_cast<int64_t>(h->num_sms));
         const dim3 g(static_cast<unsigned>(grid));
         const size_t sm = tp.smem;
         const unsigned b0 = tt::kThreads, b1 = tt::kThreads;
-        switch (tp.R * 2 + (noise ? 1 : 0)) {
-            case 16: tt::tt_conv_kernel<8, false><<<g, b0, sm, st>>>(p); break;
-            case 17: tt::tt_conv_kernel<8, true><<<g, b1, sm, st>>>(p); break;
-            case 8: tt::tt_conv_kernel<4, false><<<g, b0, sm, st>>>(p); break;
-            case 9: tt::tt_conv_kernel<4, true><<<g, b1, sm, st>>>(p); break;
-            case 4: tt::tt_conv_kernel<2, false><<<g, b0, sm, st>>>(p); break;
-            default: tt::tt_conv_kernel<2, true><<<g, b1, sm, st>>>(p); break;
+        // the general variant only when a group sum or sparse offsets are in play
+        const bool gen = ar.agg || sparse;
+        switch (tp.R * 4 + (noise ? 2 : 0) + (gen ? 1 : 0)) {
+            case 32: tt::tt_conv_kernel<8, false, false><<<g, b0, sm, st>>>(p); break;
+            case 33: tt::tt_conv_kernel<8, false, true><<<g, b0, sm, st>>>(p); break;
+            case 34: tt::tt_conv_kernel<8, true, false><<<g, b1, sm, st>>>(p); break;
+            case 35: tt::tt_conv_kernel<8, true, true><<<g, b1, sm, st>>>(p); break;
+            case 16: tt::tt_conv_kernel<4, false, false><<<g, b0, sm, st>>>(p); break;
+            case 17: tt::tt_conv_kernel<4, false, true><<<g, b0, sm, st>>>(p); break;
+            case 18: tt::tt_conv_kernel<4, true, false><<<g, b1, sm, st>>>(p); break;
+            case 19: tt::tt_conv_kernel<4, true, true><<<g, b1, sm, st>>>(p); break;
+            case 8: tt::tt_conv_kernel<2, false, false><<<g, b0, sm, st>>>(p); break;
+            case 9: tt::tt_conv_kernel<2, false, true><<<g, b0, sm, st>>>(p); break;
+            case 10: tt::tt_conv_kernel<2, true, false><<<g, b1, sm, st>>>(p); break;
+            default: tt::tt_conv_kernel<2, true, true><<<g, b1, sm, st>>>(p); break;
         }
         if (ar.agg && nchunks > 1) {
             const int64_t tot = static_cast<int64_t>(ngroups) * n;
@@ -368,6 +391,8 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->xoff);
     cudaFree(h->tab);
     cudaFree(h->in_row);
+    cudaFree(h->sring);
+    cudaFree(h->soff);
     cudaFree(h->agg_scratch);
     cudaFree(h->load_stage);
     cudaFree(h->stage);
@@ -489,6 +514,21 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     return TT_OK;
 }
 
+namespace {
+// NEXT f2: (re)select the top-n taps of dense ring rows [k_first, k_first + rows)
+tt_status select_rows(tt_channel_s* h, int64_t k_first, int64_t rows, cudaStream_t st) {
+    if (h->top_n <= 0 || rows <= 0) return TT_OK;
+    const int warps = 4;
+    const size_t sm = static_cast<size_t>(warps) * h->L * sizeof(float);
+    const int64_t nrow = static_cast<int64_t>(h->C) * rows;
+    const int64_t grid = std::min<int64_t>((nrow + warps - 1) / warps, int64_t(h->num_sms) * 16);
+    tt::tt_select_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), warps * 32, sm, st>>>(
+        h->ring, h->sring, h->soff, h->xoff, h->C, h->cap, h->L, h->L4, h->top_n, h->n4, k_first, rows);
+    TT_CUDA(cudaGetLastError(), "top-n selection launch");
+    return TT_OK;
+}
+}  // namespace
+
 tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t first_index, int64_t count,
                                     tt_stream_t stream) {
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
@@ -525,6 +565,12 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
     tt::tt_load_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), 256, 0, st>>>(
         src, count, first_index, h->ring, h->cap, h->perm, h->C, h->L, fix_prev);
     TT_CUDA(cudaGetLastError(), "snapshot loader launch");
+    {
+        // sparse rows follow the dense rows they are selected from (the previous row's
+        // difference was just completed by fix_prev)
+        tt_status ss = select_rows(h, first_index - fix_prev, count + fix_prev, st);
+        if (ss != TT_OK) return ss;
+    }
     const int64_t lo = first_index, hi = first_index + count;
     if (h->res_hi > h->res_lo && lo >= h->res_lo && lo <= h->res_hi) {
         h->res_hi = std::max(h->res_hi, hi);
@@ -613,6 +659,44 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
     return TT_OK;
 }
 
+tt_status tt_channel_set_top_n(tt_channel_t h, int32_t top_n) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    if (top_n < 0) return fail(TT_ERR_INVALID_ARG, "top_n must be >= 0");
+    DeviceGuard dg(h->dev);
+    const int32_t n = (top_n == 0 || top_n >= h->L) ? 0 : top_n;
+    if (n == h->top_n) return TT_OK;
+    TT_CUDA(cudaDeviceSynchronize(), "top-n drain");
+    cudaFree(h->sring);
+    cudaFree(h->soff);
+    h->sring = nullptr;
+    h->soff = nullptr;
+    h->top_n = 0;
+    h->n4 = 0;
+    if (n > 0) {
+        const int32_t n4 = (n + 1 + 3) & ~3;
+        TT_CUDA(cudaMalloc(&h->sring, (static_cast<size_t>(h->C) * h->cap * n + 1) * sizeof(float4)),
+                "cudaMalloc(sparse ring)");
+        TT_CUDA(cudaMalloc(&h->soff, static_cast<size_t>(h->C) * h->cap * n4 * sizeof(int32_t)),
+                "cudaMalloc(sparse offsets)");
+        TT_CUDA(cudaMemset(h->sring, 0, (static_cast<size_t>(h->C) * h->cap * n + 1) * sizeof(float4)), "zero ring");
+        TT_CUDA(cudaMemset(h->soff, 0, static_cast<size_t>(h->C) * h->cap * n4 * sizeof(int32_t)), "zero offsets");
+        h->top_n = n;
+        h->n4 = n4;
+        if (h->L * sizeof(float) * 4 > 48 * 1024)
+            TT_CUDA(cudaFuncSetAttribute(tt::tt_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(h->L * sizeof(float) * 4)),
+                    "selection smem");
+    }
+    cudaError_t e = prepare_plan(h);
+    if (e != cudaSuccess) return cuda_fail(e, "plan");
+    if (h->top_n > 0 && h->res_hi > h->res_lo) {
+        tt_status s = select_rows(h, h->res_lo, h->res_hi - h->res_lo, nullptr);
+        if (s != TT_OK) return s;
+    }
+    TT_CUDA(cudaDeviceSynchronize(), "top-n selection");
+    return TT_OK;
+}
+
 tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t num_rows) {
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
     DeviceGuard dg(h->dev);
@@ -620,6 +704,8 @@ tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t 
         if (h->in_row) {
             TT_CUDA(cudaDeviceSynchronize(), "input map drain");
             cudaFree(h->in_row);
+    cudaFree(h->sring);
+    cudaFree(h->soff);
         }
         h->in_row = nullptr;
         h->in_rows = 0;
@@ -704,6 +790,7 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
                                               h->load_stage_elems * sizeof(float2) +
                                               h->agg_scratch_elems * sizeof(float2));
     info->kernel = h->plan.kind;
+    info->top_n = h->top_n;
     info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? tt::rw::R
                                : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R : 0;
     info->launches_per_apply = h->plan.kind == TT_KERNEL_GENERIC ? 2 : 1;

@@ -55,6 +55,8 @@ struct ConvParams {
     float2* hist_wr;        // [C][H]  written with the new history
     const float4* ring;     // [C][cap][L] (g_k, g_{k+1} - g_k), taps sorted by delay
     const int32_t* xoff;    // [C][L4] window offset H - d_j of sorted tap j (pads: 0)
+    const int32_t* xoff_rows;  // NEXT f2 sparse: [C][cap][L4] offsets of each interval's selected
+                               // taps (then `ring` holds [C][cap][L] compacted rows, L = top-n); or nullptr
     int64_t n;              // samples per channel in this call
     int64_t t;              // global index of the call's first sample
     int64_t cap;            // ring slots per channel
@@ -169,12 +171,19 @@ struct SuperInfo {
     int32_t c_first;  // absolute channel of the chunk's first member
     int32_t kcount;   // channels in the chunk
 };
-__device__ __forceinline__ SuperInfo super_info(const ConvParams& p, int64_t su) {
+// 32-bit index math (the host keeps total_super < 2^31)
+__device__ __forceinline__ SuperInfo super_info(const ConvParams& p, int64_t su64) {
     SuperInfo si;
-    const int64_t rest = su / p.tiles_per_ch;
-    si.tl = static_cast<int32_t>(su - rest * p.tiles_per_ch);
-    si.g = static_cast<int32_t>(rest / p.nchunks);
-    si.q = static_cast<int32_t>(rest - static_cast<int64_t>(si.g) * p.nchunks);
+    const uint32_t su = static_cast<uint32_t>(su64);
+    const uint32_t rest = su / static_cast<uint32_t>(p.tiles_per_ch);
+    si.tl = static_cast<int32_t>(su - rest * static_cast<uint32_t>(p.tiles_per_ch));
+    if (p.nchunks == 1) {
+        si.g = static_cast<int32_t>(rest);
+        si.q = 0;
+    } else {
+        si.g = static_cast<int32_t>(rest / static_cast<uint32_t>(p.nchunks));
+        si.q = static_cast<int32_t>(rest - static_cast<uint32_t>(si.g) * static_cast<uint32_t>(p.nchunks));
+    }
     si.c_first = p.c_lo + si.g * p.group + si.q * p.chunk;
     const int32_t left = p.group - si.q * p.chunk;
     si.kcount = left < p.chunk ? left : p.chunk;
@@ -229,21 +238,32 @@ __device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo
     const Piece c1 = make_piece(st.coef, ringc + s0 * p.L, static_cast<uint32_t>(r1) * rowb);
     const Piece c2 = make_piece(st.coef + static_cast<int64_t>(r1) * p.L, ringc,
                                 static_cast<uint32_t>(ti.nk - r1) * rowb);
-    // E: tap offsets of this channel
-    const Piece e = make_piece(st.xo, p.xoff + static_cast<int64_t>(ti.c) * p.L4, static_cast<uint32_t>(p.L4) * 4u);
+    // E, F: tap offsets — the channel's row, or (sparse) one row per staged interval
+    Piece e, f;
+    const uint32_t xrowb = static_cast<uint32_t>(p.L4) * 4u;
+    if (p.xoff_rows) {
+        const int32_t* xr = p.xoff_rows + static_cast<int64_t>(ti.c) * p.cap * p.L4;
+        e = make_piece(st.xo, xr + s0 * p.L4, static_cast<uint32_t>(r1) * xrowb);
+        f = make_piece(st.xo + static_cast<int64_t>(r1) * p.L4, xr, static_cast<uint32_t>(ti.nk - r1) * xrowb);
+    } else {
+        e = make_piece(st.xo, p.xoff + static_cast<int64_t>(ti.c) * p.L4, xrowb);
+        f = make_piece(st.xo, p.xoff, 0u);
+    }
     piece_plain(a, lane);
     piece_plain(bx, lane);
     piece_plain(c1, lane);
     piece_plain(c2, lane);
     piece_plain(e, lane);
+    piece_plain(f, lane);
     __syncwarp();  // the lanes' plain stores happen-before lane 0's release (arrive)
     if (lane == 0) {
-        mbar_arrive_expect_tx(full, a.body + bx.body + c1.body + c2.body + e.body);
+        mbar_arrive_expect_tx(full, a.body + bx.body + c1.body + c2.body + e.body + f.body);
         piece_tma(a, full);
         piece_tma(bx, full);
         piece_tma(c1, full);
         piece_tma(c2, full);
         piece_tma(e, full);
+        piece_tma(f, full);
     }
 }
 
@@ -271,7 +291,7 @@ __device__ __forceinline__ void mac_tap(const float4 q, const float2* __restrict
 // reads per tap instead of one per row.
 template <int R, int NG>
 __device__ __forceinline__ void mac_tap_grouped(const float4* __restrict__ cf, int32_t L, int32_t j,
-                                                const float2* __restrict__ xp, const float (&alpha)[R],
+                                                const float2* const (&xp)[NG], const float (&alpha)[R],
                                                 float2 (&A)[R], float2 (&B)[R]) {
     constexpr int RPG = R / NG;
     float4 q[NG];
@@ -279,7 +299,7 @@ __device__ __forceinline__ void mac_tap_grouped(const float4* __restrict__ cf, i
     for (int g = 0; g < NG; ++g) q[g] = cf[g * L + j];
     float2 xv[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+    for (int r = 0; r < R; ++r) xv[r] = xp[r / RPG][r * 32];
     float2 h[R];
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -292,18 +312,32 @@ __device__ __forceinline__ void mac_tap_grouped(const float4* __restrict__ cf, i
     }
 }
 
-template <int R, int NG>
+// ROWS: (sparse) each interval has its own tap offsets row; else all share row 0
+template <int R, int NG, bool ROWS>
 __device__ __forceinline__ void taps_grouped(const ConvParams& p, const float4* cf, const int32_t* xo,
                                              const float2* xb, const float (&alpha)[R], float2 (&A)[R],
                                              float2 (&B)[R]) {
 #pragma unroll 2
-    for (int32_t j = 0; j < p.L; ++j) mac_tap_grouped<R, NG>(cf, p.L, j, xb + xo[j], alpha, A, B);
+    for (int32_t j = 0; j < p.L; ++j) {
+        const float2* xp[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) xp[g] = xb + (ROWS ? xo[g * p.L4 + j] : xo[j]);
+        mac_tap_grouped<R, NG>(cf, p.L, j, xp, alpha, A, B);
+    }
+}
+template <int R, int NG>
+__device__ __forceinline__ void taps_grouped_rt(const ConvParams& p, const float4* cf, const int32_t* xo,
+                                                const float2* xb, const float (&alpha)[R], float2 (&A)[R],
+                                                float2 (&B)[R]) {
+    if (p.xoff_rows) taps_grouped<R, NG, true>(p, cf, xo, xb, alpha, A, B);
+    else taps_grouped<R, NG, false>(p, cf, xo, xb, alpha, A, B);
 }
 
-// Consumer warp: the 32R outputs of warp `cw` in tile `ti`.
-template <int R, bool NOISE>
+// Consumer warp: the 32R outputs of warp `cw` in tile `ti`. GEN: the general variant
+// (group sums, sparse per-interval offsets); the plain variant compiles none of it.
+template <int R, bool NOISE, bool GEN>
 __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
-                                             int lane, bool first, float2 (&acc)[R]) {
+                                             int lane, bool first, float2* aggdst) {
     const int32_t obase = cw * 32 * R + lane;
     if (cw * 32 * R < ti.Tt) {
         // per-output interpolation weight alpha = j / S (a multiply when S is a power of
@@ -331,9 +365,12 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
         const uint32_t wj0 = static_cast<uint32_t>(ti.j0 + cw * 32 * R);
         const uint32_t kw0 = div_S(p, wj0);
         const uint32_t kw1 = div_S(p, wj0 + 32 * R - 1);
+        // tap offsets of interval kk: one row per interval when sparse, else the channel's
+        const int32_t xo_row = (GEN && p.xoff_rows) ? p.L4 : 0;
         if (kw0 == kw1) {
             const float4* cf = st.coef + static_cast<int64_t>(kw0) * p.L;
-            const int4* xo4 = reinterpret_cast<const int4*>(st.xo);
+            const int32_t* xo = st.xo + kw0 * xo_row;
+            const int4* xo4 = reinterpret_cast<const int4*>(xo);
             int32_t j = 0;
             int4 o4 = xo4[0];
             for (; j + 4 <= p.L; j += 4) {
@@ -345,22 +382,27 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
                 mac_tap<R>(q2, xb + o.z, alpha, A, B);
                 mac_tap<R>(q3, xb + o.w, alpha, A, B);
             }
-            for (; j < p.L; ++j) mac_tap<R>(cf[j], xb + st.xo[j], alpha, A, B);
-        } else if ((R & (R - 1)) == 0 && p.s_shift >= 5 && (32 * R) % p.S == 0 && (wj0 & (p.S - 1)) == 0) {
-            // the warp starts on an interval boundary and spans NG = 32R / S whole intervals
+            for (; j < p.L; ++j) mac_tap<R>(cf[j], xb + xo[j], alpha, A, B);
+        } else if ((R & (R - 1)) == 0 && p.s_shift >= 5 && (32 * R) % p.S == 0 && (wj0 & (p.S - 1)) == 0 &&
+                   ((32 * R) >> p.s_shift) <= 4 &&
+                   static_cast<int32_t>(kw0) + ((32 * R) >> p.s_shift) <= ti.nk) {  // (tail tiles: rows staged)
+            // the warp starts on an interval boundary and spans NG = 32R / S (2 or 4) whole intervals
             const float4* cf = st.coef + static_cast<int64_t>(kw0) * p.L;
-            switch ((32 * R) >> p.s_shift) {
-                case 2: taps_grouped<R, (R >= 2 ? 2 : 1)>(p, cf, st.xo, xb, alpha, A, B); break;
-                case 4: taps_grouped<R, (R >= 4 ? 4 : 1)>(p, cf, st.xo, xb, alpha, A, B); break;
-                default: taps_grouped<R, R>(p, cf, st.xo, xb, alpha, A, B); break;
+            const int32_t* xo = st.xo + kw0 * xo_row;
+            if constexpr (GEN) {
+                if (((32 * R) >> p.s_shift) == 2) taps_grouped_rt<R, (R >= 2 ? 2 : 1)>(p, cf, xo, xb, alpha, A, B);
+                else taps_grouped_rt<R, (R >= 4 ? 4 : 1)>(p, cf, xo, xb, alpha, A, B);
+            } else {
+                if (((32 * R) >> p.s_shift) == 2) taps_grouped<R, (R >= 2 ? 2 : 1), false>(p, cf, xo, xb, alpha, A, B);
+                else taps_grouped<R, (R >= 4 ? 4 : 1), false>(p, cf, xo, xb, alpha, A, B);
             }
         } else {
             for (int32_t j = 0; j < p.L; ++j) {
-                const float2* xp = xb + st.xo[j];
+                const float2* xp = xb + st.xo[j];  // dense: one offset row
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const float4 q = st.coef[kk[r] * p.L + j];
-                    const float2 xv = xp[r * 32];
+                    const float2 xv = (GEN && xo_row) ? xb[st.xo[kk[r] * xo_row + j] + r * 32] : xp[r * 32];
                     const float2 h =
                         __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w), make_float2(q.x, q.y));
                     A[r] = __ffma2_rn(make_float2(h.x, h.x), xv, A[r]);
@@ -415,11 +457,21 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
                 if (o < ti.Tt) yc[o] = out[r];
             }
         }
-        if (p.agg) {
-            // running chunk sum in channel order: acc = y_first, then acc += y_k
+        if (GEN && aggdst) {
+            // running chunk sum in channel order, kept in the destination row itself (each
+            // element is read back only by the thread that wrote it): s = y_first, s += y_k
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-                acc[r] = first ? out[r] : make_float2(__fadd_rn(acc[r].x, out[r].x), __fadd_rn(acc[r].y, out[r].y));
+            for (int r = 0; r < R; ++r) {
+                const int32_t o = obase + r * 32;
+                if (o < ti.Tt) {
+                    if (first) {
+                        aggdst[o] = out[r];
+                    } else {
+                        const float2 v = aggdst[o];
+                        aggdst[o] = make_float2(__fadd_rn(v.x, out[r].x), __fadd_rn(v.y, out[r].y));
+                    }
+                }
+            }
         }
     }
     // the tile that ends the call writes the new delay-line history (ping-pong); the
@@ -430,17 +482,17 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
     }
 }
 
-template <int R, bool NOISE>
+template <int R, bool NOISE, bool GEN>
 __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p) {
     constexpr int T = kConsumerWarps * 32 * R;
     extern __shared__ __align__(128) unsigned char smem[];
     // layout: [full kMaxStages x 8 B | empty kMaxStages x 8 B | pad to 128][stage 0][stage 1]...
-    //   stage = [win (H+T) float2][coef nk_max x L float4][xo L4 int32]
+    //   stage = [win (H+T) float2][coef nk_max x L float4][xo (sparse: nk_max x) L4 int32]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
     const int64_t WB = static_cast<int64_t>(p.H + T) * 8;
     const int64_t CB = static_cast<int64_t>(p.nk_max) * p.L * 16;
-    const int64_t SB = WB + CB + static_cast<int64_t>(p.L4) * 4;
+    const int64_t SB = WB + CB + static_cast<int64_t>(p.xoff_rows ? p.nk_max : 1) * p.L4 * 4;
     auto stage = [&](int s) {
         unsigned char* base = smem + 128 + s * SB;
         Stage st;
@@ -462,40 +514,57 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
     if (warp == kConsumerWarps) {
         // producer: run ahead of the consumers by up to `stages` tiles
         int it = 0;
-        for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
-            const SuperInfo si = super_info(p, su);
-            for (int32_t k = 0; k < si.kcount; ++k, ++it) {
+        if constexpr (!GEN) {
+            // one channel tile per work item: w -> (channel, tile)
+            for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
                 const int s = it % p.stages;
                 const int kk = it / p.stages;
                 if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
-                produce_tile<R>(p, tile_info<R>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
+                const uint32_t cl = static_cast<uint32_t>(w) / static_cast<uint32_t>(p.tiles_per_ch);
+                const int32_t tl = static_cast<int32_t>(static_cast<uint32_t>(w) - cl * p.tiles_per_ch);
+                produce_tile<R>(p, tile_info<R>(p, p.c_lo + static_cast<int32_t>(cl), tl), stage(s), &full[s], lane);
+            }
+        } else {
+            for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
+                const SuperInfo si = super_info(p, su);
+                for (int32_t k = 0; k < si.kcount; ++k, ++it) {
+                    const int s = it % p.stages;
+                    const int kk = it / p.stages;
+                    if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
+                    produce_tile<R>(p, tile_info<R>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
+                }
             }
         }
     } else {
-        const int32_t obase = warp * 32 * R + lane;
         int it = 0;
+        if constexpr (!GEN) {
+            for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
+                const int s = it % p.stages;
+                const int kk = it / p.stages;
+                mbar_wait(&full[s], kk & 1);
+                const uint32_t cl = static_cast<uint32_t>(w) / static_cast<uint32_t>(p.tiles_per_ch);
+                const int32_t tl = static_cast<int32_t>(static_cast<uint32_t>(w) - cl * p.tiles_per_ch);
+                const TileInfo ti = tile_info<R>(p, p.c_lo + static_cast<int32_t>(cl), tl);
+                consume_tile<R, NOISE, false>(p, ti, stage(s), warp, lane, true, nullptr);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            return;
+        }
         for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
             const SuperInfo si = super_info(p, su);
-            float2 acc[R];
-            TileInfo ti;
             for (int32_t k = 0; k < si.kcount; ++k, ++it) {
                 const int s = it % p.stages;
                 const int kk = it / p.stages;
                 mbar_wait(&full[s], kk & 1);
-                ti = tile_info<R>(p, si.c_first + k, si.tl);
-                consume_tile<R, NOISE>(p, ti, stage(s), warp, lane, k == 0, acc);
+                const TileInfo ti = tile_info<R>(p, si.c_first + k, si.tl);
+                // the chunk's sum goes straight into the group row, or into its partial row
+                float2* aggdst = (GEN && p.agg)
+                                     ? p.agg + (static_cast<int64_t>(si.g) * p.nchunks + si.q) * p.n + ti.i0
+                                     : nullptr;
+                consume_tile<R, NOISE, GEN>(p, ti, stage(s), warp, lane, k == 0, aggdst);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
-            }
-            if (p.agg && warp * 32 * R < ti.Tt) {
-                // the chunk's sum: straight into the group row, or into its partial row
-                float2* dst = p.agg + (static_cast<int64_t>(si.g) * (p.nchunks > 1 ? p.nchunks : 1) +
-                                       (p.nchunks > 1 ? si.q : 0)) * p.n + ti.i0;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int32_t o = obase + r * 32;
-                    if (o < ti.Tt) dst[o] = acc[r];
-                }
             }
         }
     }
@@ -517,10 +586,11 @@ __global__ void __launch_bounds__(256) tt_conv_generic_kernel(const ConvParams p
         const int64_t k = n / p.S;
         const int32_t jj = static_cast<int32_t>(n - k * p.S);
         const float alpha = __fdiv_rn(__uint2float_rn(static_cast<uint32_t>(jj)), __int2float_rn(p.S));
-        const float4* cr = p.ring + (static_cast<int64_t>(c) * p.cap + (k % p.cap)) * p.L;
+        const int64_t rowi = static_cast<int64_t>(c) * p.cap + (k % p.cap);
+        const float4* cr = p.ring + rowi * p.L;
         const float2* xc = p.x + (p.in_row ? static_cast<int64_t>(__ldg(p.in_row + c)) : cl) * p.n;
         const float2* hc = p.hist_rd + static_cast<int64_t>(c) * p.H;
-        const int32_t* xo = p.xoff + static_cast<int64_t>(c) * p.L4;
+        const int32_t* xo = p.xoff_rows ? p.xoff_rows + rowi * p.L4 : p.xoff + static_cast<int64_t>(c) * p.L4;
         float2 A = make_float2(0.f, 0.f), Bv = make_float2(0.f, 0.f);
         for (int32_t j = 0; j < p.L; ++j) {
             const float4 q = __ldg(cr + j);
@@ -587,6 +657,57 @@ __global__ void tt_group_sum_kernel(const float2* __restrict__ src, float2* __re
             s = q == 0 ? pq : make_float2(__fadd_rn(s.x, pq.x), __fadd_rn(s.y, pq.y));
         }
         agg[e] = s;
+    }
+}
+
+// NEXT f2 selection + compaction ("top-n dominant taps at each time step";
+// DESIGN.md R20): for each staged snapshot row (c, k) of the dense ring, keep the n taps
+// of largest m_j = fl(fl(g.re g.re) + fl(g.im g.im)) — ties to the smaller sorted index j
+// (= smaller delay, then smaller original index) — and write them, in ascending delay
+// order, with their (g, dg) and window offsets into the sparse ring. One warp per row:
+// the row's magnitudes go to shared memory, each lane ranks its taps against all L,
+// and a ballot prefix count gives each selected tap its compacted slot.
+__global__ void tt_select_kernel(const float4* __restrict__ ring, float4* __restrict__ sring,
+                                 int32_t* __restrict__ soff, const int32_t* __restrict__ xoff, int32_t C, int64_t cap,
+                                 int32_t L, int32_t L4, int32_t n, int32_t n4, int64_t k_first, int64_t rows) {
+    extern __shared__ float mags[];  // [warps per block][L]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* m = mags + warp * L;
+    const int64_t nrow = static_cast<int64_t>(C) * rows;
+    for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp; row < nrow;
+         row += static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5)) {
+        const int64_t c = row / rows;
+        const int64_t slot = (k_first + (row - c * rows)) % cap;
+        const float4* src = ring + (c * cap + slot) * L;
+        for (int32_t j = lane; j < L; j += 32) {
+            const float4 q = src[j];
+            m[j] = __fadd_rn(__fmul_rn(q.x, q.x), __fmul_rn(q.y, q.y));
+        }
+        __syncwarp();
+        float4* dst = sring + (c * cap + slot) * n;
+        int32_t* od = soff + (c * cap + slot) * n4;
+        int32_t base = 0;  // selected taps before this 32-tap chunk
+        for (int32_t j0 = 0; j0 < L; j0 += 32) {
+            const int32_t j = j0 + lane;
+            bool sel = false;
+            if (j < L) {
+                const float mj = m[j];
+                int32_t rank = 0;
+                for (int32_t i = 0; i < L; ++i) {
+                    const float mi = m[i];
+                    rank += (mi > mj || (mi == mj && i < j)) ? 1 : 0;
+                }
+                sel = rank < n;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+            if (sel) {
+                const int32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                dst[pos] = src[j];
+                od[pos] = __ldg(xoff + c * L4 + j);
+            }
+            base += __popc(bal);
+        }
+        __syncwarp();
     }
 }
 

@@ -124,3 +124,60 @@ def test_input_map_plain_apply_and_errors(cuda_device):
     ch.close()
     run.x = xg[rows]
     compare(y, run.oracle(), "mapped apply")
+
+
+def _run_sparse(run, device, top_n, calls, set_before_load=True):
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    ch = Channel(run.delays, run.w.S, seed=run.seed, snapshot_capacity=run.K, channel_offset=run.c_lo, device=device)
+    try:
+        if set_before_load:
+            ch.set_top_n(top_n)
+        ch.load_snapshots(torch.from_numpy(run.gains).to(device), 0)
+        if not set_before_load:
+            ch.set_top_n(top_n)
+        assert ch.info().top_n == (top_n if 0 < top_n < run.w.L else 0)
+        out, pos = [], 0
+        for n in calls:
+            xs = torch.from_numpy(np.ascontiguousarray(run.x[:, pos:pos + n])).to(device)
+            out.append(ch.apply(xs, noise_sigma=run.sigma).cpu().numpy())
+            pos += n
+        torch.cuda.synchronize()
+    finally:
+        ch.close()
+    return np.concatenate(out, axis=1)
+
+
+@pytest.mark.parametrize("name,kw,top_n", [
+    ("c4", dict(ues=2, n_per_call=12_000, calls=1), 20),        # one interval per warp (S=256, R=8)
+    ("c4", dict(ues=2, n_per_call=12_000, calls=1), 1),
+    ("c5-L64", dict(ues=2, n_per_call=9_000), 16),               # S=128: two intervals per warp
+    ("c3", dict(ues=2, n_per_call=8_000, calls=1), 10),
+    ("c2", dict(ues=2, n_per_call=5_000), 22),
+])
+def test_sparse_top_n_parity(cuda_device, name, kw, top_n):
+    """f2: each interval sums its top-n taps; oracle parity (same float32
+    selection rule), any call split bit-identical, tiled == generic bit for bit."""
+    w = ttsynth.get(name).scaled(**kw)
+    run = Run(w, seed=13)
+    N = run.N
+    y = _run_sparse(run, cuda_device, top_n, [N])
+    ref = oracle.convolve(run.delays, w.S, run.gains, 0, run.x, 0, 0, N, sigma=run.sigma, seed=run.seed,
+                          top_n=top_n)
+    compare(y, ref, f"{name} top-{top_n}")
+    assert np.array_equal(_run_sparse(run, cuda_device, top_n, [N // 3, 7, N - N // 3 - 7]), y)
+    assert np.array_equal(_run_sparse(run, cuda_device, top_n, [N], set_before_load=False), y)
+
+
+def test_sparse_n_equal_L_is_dense_and_generic_path(cuda_device, monkeypatch):
+    w = ttsynth.get("c4").scaled(ues=2, n_per_call=9_000, calls=1)
+    run = Run(w, seed=2)
+    dense = run.gpu(cuda_device)
+    assert np.array_equal(_run_sparse(run, cuda_device, w.L, [run.N]), dense)
+    assert np.array_equal(_run_sparse(run, cuda_device, 0, [run.N]), dense)
+    sp = _run_sparse(run, cuda_device, 17, [run.N])
+    monkeypatch.setenv("TT_KERNEL", "generic")
+    assert np.array_equal(_run_sparse(run, cuda_device, 17, [run.N]), sp)
+    monkeypatch.delenv("TT_KERNEL")

@@ -22,5 +22,6 @@ from .oracle import (  # noqa: F401
     convolve_points,
     aggregate,
     select_top_n,
+    synth_jakes,
     OracleError,
 )

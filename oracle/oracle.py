@@ -55,6 +55,8 @@ def lib() -> ct.CDLL:
             L.tto_convolve_topn.restype = ct.c_int
             L.tto_select_top_n.argtypes = [i32, P, P, i32, P]
             L.tto_select_top_n.restype = None
+            L.tto_synth_jakes.argtypes = [i32, i32, P, P, i32, ct.c_double, u64, i64, i64, i64, P, P]
+            L.tto_synth_jakes.restype = None
             L.tto_convolve_points.argtypes = [i32, i32, P, i32, P, i64, i64, P, i64, i64, P, P, i64, f32,
                                               u64, i64, P]
             L.tto_convolve_points.restype = ct.c_int
@@ -176,3 +178,18 @@ def select_top_n(delays_row, g_row, n: int) -> np.ndarray:
     sel = np.zeros(len(d), dtype=np.uint8)
     lib().tto_select_top_n(len(d), _ptr(d), _ptr(g), int(n), _ptr(sel))
     return sel.astype(bool)
+
+
+def synth_jakes(tau, power, M: int, nu: float, seed: int, k0: int, K: int, c_offset: int = 0):
+    """NEXT f3: Jakes sum-of-sinusoids snapshots on the integer delay grid (see
+    tt_oracle.c tto_synth_jakes). tau, power: [C][P] path delays (samples) and powers.
+    nu = f_D S / f_s (cycles per snapshot). Returns (delays int32 [C][2P],
+    gains float32 [C][K][2P][2]) for snapshots k0 .. k0+K-1."""
+    t = np.ascontiguousarray(tau, dtype=np.float32)
+    w = np.ascontiguousarray(power, dtype=np.float32)
+    C, P = t.shape
+    d = np.zeros((C, 2 * P), np.int32)
+    g = np.zeros((C, K, 2 * P, 2), np.float32)
+    lib().tto_synth_jakes(C, P, _ptr(t), _ptr(w), int(M), float(nu), int(seed), int(c_offset), int(k0), int(K),
+                          _ptr(d), _ptr(g))
+    return d, g

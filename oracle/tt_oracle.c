@@ -307,3 +307,61 @@ int tto_convolve_points(int32_t C, int32_t L, const int32_t* delays, int32_t S, 
     }
     return err;
 }
+
+/* ---------------------------------------------------------------------------
+ * NEXT f3: channel-state synthesis (§IV: traces are "discrete complex tap
+ * values over time" resampled "onto a fixed delay grid"; 3GPP PDPs with "time variation
+ * synthesized via a Jakes-based Doppler model"). DESIGN.md reading R21, step by step:
+ *   path p of channel c: fractional delay tau_p >= 0 (samples), power w_p;
+ *   random numbers: Philox4x32-10 key (seed lo, seed hi),
+ *     u_p      = U(word 1 of Philox(ctr = (0, p, c_g, 0x5EEDF3)))   angle offset
+ *     phi_{p,m}= U(word 0 of Philox(ctr = (m, p, c_g, 0x5EEDF3)))   phase (revolutions)
+ *     U(w) = (w >> 8) 2^-24 in [0, 1);
+ *   theta_{p,m} = 2 pi (m + u_p) / M (M arrival angles, Clarke sum of sinusoids);
+ *   nu = f_D S / f_s: Doppler in cycles per snapshot period;
+ *   a_p(k) = M^-1/2 sum_m exp(j 2 pi (nu cos(theta_{p,m}) k + phi_{p,m}))
+ *   g_p(k) = sqrt(w_p) a_p(k);
+ *   two-bin split onto the integer grid: b = floor(tau_p), f = tau_p - b,
+ *     tap 2p at delay b gets (1 - f) g_p(k), tap 2p+1 at delay b + 1 gets f g_p(k).
+ * Everything in double; outputs rounded to float32 once.
+ * ------------------------------------------------------------------------- */
+static double u01(uint32_t w) { return (double)(w >> 8) * (1.0 / 16777216.0); }
+
+void tto_synth_jakes(int32_t C, int32_t P, const float* tau /* [C][P] */, const float* pw /* [C][P] */,
+                     int32_t M, double nu, uint64_t seed, int64_t c_offset, int64_t k0, int64_t K,
+                     int32_t* delays /* [C][2P] */, float* gains /* [C][K][2P][2] */) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const double PI = 3.14159265358979323846;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t c = 0; c < C; ++c) {
+        const uint32_t cg = (uint32_t)(c_offset + c);
+        for (int32_t p = 0; p < P; ++p) {
+            const double t = tau[c * P + p];
+            const double b = floor(t), f = t - b;
+            delays[(int64_t)c * 2 * P + 2 * p] = (int32_t)b;
+            delays[(int64_t)c * 2 * P + 2 * p + 1] = (int32_t)b + 1;
+            uint32_t ctr[4] = {0u, (uint32_t)p, cg, 0x5EEDF3u}, r[4];
+            tto_philox4x32_10(ctr, key, r);
+            const double up = u01(r[1]);
+            const double amp = sqrt((double)pw[c * P + p] / (double)M);
+            for (int64_t k = 0; k < K; ++k) {
+                double ar = 0.0, ai = 0.0;
+                for (int32_t m = 0; m < M; ++m) {
+                    uint32_t cm[4] = {(uint32_t)m, (uint32_t)p, cg, 0x5EEDF3u}, rm[4];
+                    tto_philox4x32_10(cm, key, rm);
+                    const double phi = u01(rm[0]);
+                    const double th = 2.0 * PI * ((double)m + up) / (double)M;
+                    const double ph = 2.0 * PI * (nu * cos(th) * (double)(k0 + k) + phi);
+                    ar += cos(ph);
+                    ai += sin(ph);
+                }
+                const double gr = amp * ar, gi = amp * ai;
+                float* row = gains + (((int64_t)c * K + k) * 2 * P) * 2;
+                row[4 * p] = (float)((1.0 - f) * gr);
+                row[4 * p + 1] = (float)((1.0 - f) * gi);
+                row[4 * p + 2] = (float)(f * gr);
+                row[4 * p + 3] = (float)(f * gi);
+            }
+        }
+    }
+}

@@ -171,6 +171,26 @@ tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t 
 tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out, float* agg, int32_t group_size,
                                      int64_t n_samples, float noise_sigma, tt_stream_t stream);
 
+/* NEXT f3 (§IV: traces of "discrete complex tap values over time" on "a fixed
+ * delay grid", 3GPP PDPs "with time variation synthesized via a Jakes-based Doppler
+ * model"): synthesise gain snapshots first_index .. first_index+count-1 on the GPU, in
+ * the layout tt_channel_load_snapshots takes (R21):
+ *   path p of channel c: delay tau = path_delay[c][p] samples (fractional allowed, in
+ *   [0, TT_MAX_DELAY - 1]), power w = path_power[c][p]; Jakes/Clarke sum of M =
+ *   num_sinusoids sinusoids with arrival angles 2 pi (m + u_p) / M and Philox-drawn
+ *   phases (key seed, counter (m, p, channel_offset + c, 0x5EEDF3)); Doppler nu =
+ *   f_D S / f_s cycles per snapshot (0 <= nu < 0.5);
+ *   the path's gain is split onto grid taps 2p, 2p+1 at delays floor(tau), floor(tau)+1
+ *   with weights (1 - frac, frac) (so the handle has L = 2 num_paths taps).
+ * path_delay, path_power: host float [C][P]. delays_out: host int32 [C][2P] receives
+ * the grid delays (may be NULL). gains_out: device float [C][count][2P][2].
+ * Synchronises `stream` (temporary device tables are freed before returning).
+ * Errors: INVALID_ARG (NULL inputs, sizes, nu outside [0, 0.5), delays or powers out of
+ * range), OUT_OF_MEMORY, CUDA. */
+tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32_t num_ue, int32_t num_paths,
+                         int32_t num_sinusoids, double nu, uint64_t seed, int64_t channel_offset, int64_t first_index,
+                         int64_t count, int32_t* delays_out, float* gains_out, tt_stream_t stream);
+
 /* Same as tt_channel_apply but `in` and `out` are HOST memory (pinned for full
  * overlap; pageable works but copies synchronously). The library pipelines
  * host->device copies, the kernel and device->host copies over channel chunks on

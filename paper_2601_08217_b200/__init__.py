@@ -7,12 +7,12 @@ every compute call goes through the CUDA library.
 """
 from ._lib import TTError, tt_abi_version  # noqa: F401
 
-__all__ = ["Channel", "TTError", "tt_abi_version"]
+__all__ = ["Channel", "TTError", "tt_abi_version", "synth_jakes"]
 
 
 def __getattr__(name):
-    if name == "Channel":  # torch is imported lazily
-        from .channel import Channel
+    if name in ("Channel", "synth_jakes"):  # torch is imported lazily
+        from . import channel
 
-        return Channel
+        return getattr(channel, name)
     raise AttributeError(name)

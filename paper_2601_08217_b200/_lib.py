@@ -34,6 +34,7 @@ EXPORTS = (
     "tt_channel_set_top_n",
     "tt_channel_set_input_map",
     "tt_channel_apply_aggregate",
+    "tt_synth_jakes",
     "tt_channel_reset",
     "tt_channel_get_info",
     "tt_channel_destroy",
@@ -95,6 +96,8 @@ def lib() -> ct.CDLL:
             L.tt_channel_set_top_n.argtypes = [P, i32]
             L.tt_channel_set_input_map.argtypes = [P, P, i32]
             L.tt_channel_apply_aggregate.argtypes = [P, P, P, P, i32, i64, f32, P]
+            L.tt_synth_jakes.argtypes = [P, P, i32, i32, i32, ct.c_double, u64, i64, i64, i64, P, P, P]
+            L.tt_synth_jakes.restype = ct.c_int
             L.tt_channel_reset.argtypes = [P, P]
             L.tt_channel_get_info.argtypes = [P, ct.POINTER(ChannelInfo)]
             L.tt_channel_destroy.argtypes = [P]
@@ -150,6 +153,13 @@ def tt_channel_set_input_map(h: int, rows_ptr: int, num_rows: int) -> None:
 def tt_channel_apply_aggregate(h: int, in_ptr: int, out_ptr: int, agg_ptr: int, group_size: int, n_samples: int,
                                noise_sigma: float, stream: int) -> None:
     check(lib().tt_channel_apply_aggregate(h, in_ptr, out_ptr, agg_ptr, group_size, n_samples, noise_sigma, stream))
+
+
+def tt_synth_jakes(delay_ptr: int, power_ptr: int, num_ue: int, num_paths: int, num_sinusoids: int, nu: float,
+                   seed: int, channel_offset: int, first_index: int, count: int, delays_out_ptr: int, gains_ptr: int,
+                   stream: int) -> None:
+    check(lib().tt_synth_jakes(delay_ptr, power_ptr, num_ue, num_paths, num_sinusoids, nu, seed, channel_offset,
+                               first_index, count, delays_out_ptr, gains_ptr, stream))
 
 
 def tt_channel_reset(h: int, stream: int) -> None:

@@ -164,3 +164,24 @@ class Channel:
 
     def reset(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         _lib.tt_channel_reset(self.handle, _stream_ptr(stream))
+
+
+def synth_jakes(path_delay, path_power, num_sinusoids: int, nu: float, seed: int, first_index: int, count: int,
+                channel_offset: int = 0, device=None, stream: Optional[torch.cuda.Stream] = None):
+    """NEXT f3: Jakes snapshots synthesised on the GPU (tt_synth_jakes). path_delay,
+    path_power: [C][P] (fractional delays in samples, powers). Returns (delays int32
+    numpy [C][2P], gains float32 device tensor [C][count][2P][2]) ready for
+    Channel(delays, ...) and Channel.load_snapshots(gains, first_index)."""
+    t = np.ascontiguousarray(np.asarray(path_delay, dtype=np.float32))
+    w = np.ascontiguousarray(np.asarray(path_power, dtype=np.float32))
+    if t.ndim != 2 or t.shape != w.shape:
+        raise ValueError("path_delay and path_power must both be [C][P]")
+    C, P = t.shape
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    d = np.zeros((C, 2 * P), np.int32)
+    g = torch.empty((C, int(count), 2 * P, 2), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.tt_synth_jakes(t.ctypes.data, w.ctypes.data, C, P, int(num_sinusoids), float(nu), int(seed),
+                            int(channel_offset), int(first_index), int(count), d.ctypes.data, g.data_ptr(),
+                            _stream_ptr(stream))
+    return d, g

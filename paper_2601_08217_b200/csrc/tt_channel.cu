@@ -16,6 +16,7 @@
 #include "tt_channel.h"
 #include "tt_conv.cuh"
 #include "tt_conv_rw.cuh"
+#include "tt_synth.cuh"
 
 namespace {
 
@@ -757,6 +758,68 @@ tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out
     if (s != TT_OK) return s;
     h->t += n_samples;
     if (h->H > 0) h->p ^= 1;
+    return TT_OK;
+}
+
+tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32_t num_ue, int32_t num_paths,
+                         int32_t num_sinusoids, double nu, uint64_t seed, int64_t channel_offset, int64_t first_index,
+                         int64_t count, int32_t* delays_out, float* gains_out, tt_stream_t stream) {
+    if (!path_delay || !path_power || !gains_out) return fail(TT_ERR_INVALID_ARG, "NULL path_delay/path_power/gains_out");
+    if (num_ue <= 0 || num_paths <= 0 || num_sinusoids <= 0 || count <= 0 || first_index < 0 || channel_offset < 0)
+        return fail(TT_ERR_INVALID_ARG, "need num_ue, num_paths, num_sinusoids, count > 0 and first_index, "
+                                        "channel_offset >= 0");
+    if (!(nu >= 0.0) || !(nu < 0.5)) return fail(TT_ERR_INVALID_ARG, "nu = f_D S / f_s must be in [0, 0.5) (Nyquist)");
+    const int64_t CP = static_cast<int64_t>(num_ue) * num_paths;
+    if (2 * static_cast<int64_t>(num_paths) > TT_MAX_TAPS) return fail(TT_ERR_INVALID_ARG, "2 num_paths > TT_MAX_TAPS");
+    for (int64_t i = 0; i < CP; ++i) {
+        if (!(path_delay[i] >= 0.0f) || !(path_delay[i] + 1.0f <= static_cast<float>(TT_MAX_DELAY)) ||
+            !(path_power[i] >= 0.0f) || !std::isfinite(path_power[i]))
+            return fail(TT_ERR_INVALID_ARG, "path %lld: delay must be in [0, %d - 1], power finite and >= 0",
+                        (long long)i, TT_MAX_DELAY);
+        if (delays_out) {
+            const int32_t b = static_cast<int32_t>(floorf(path_delay[i]));
+            const int64_t c = i / num_paths, p = i % num_paths;
+            delays_out[c * 2 * num_paths + 2 * p] = b;
+            delays_out[c * 2 * num_paths + 2 * p + 1] = b + 1;
+        }
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float *dtau = nullptr, *dpw = nullptr;
+    double2* tab = nullptr;
+    const size_t tab_b = static_cast<size_t>(CP) * num_sinusoids * sizeof(double2);
+    auto cleanup = [&]() {
+        cudaFree(dtau);
+        cudaFree(dpw);
+        cudaFree(tab);
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&dtau, CP * sizeof(float))) != cudaSuccess ||
+        (e = cudaMalloc(&dpw, CP * sizeof(float))) != cudaSuccess || (e = cudaMalloc(&tab, tab_b)) != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "cudaMalloc(synthesis)");
+    }
+    if ((e = cudaMemcpyAsync(dtau, path_delay, CP * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dpw, path_power, CP * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "copy paths");
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tt = CP * num_sinusoids;
+    tt::tt_synth_table_kernel<<<static_cast<unsigned>(std::min<int64_t>((tt + 255) / 256, int64_t(sms) * 16)), 256, 0,
+                                st>>>(num_ue, num_paths, num_sinusoids, nu, static_cast<uint32_t>(seed),
+                                      static_cast<uint32_t>(seed >> 32), channel_offset, tab);
+    const int64_t tg = CP * count;
+    tt::tt_synth_gain_kernel<<<static_cast<unsigned>(std::min<int64_t>((tg + 255) / 256, int64_t(sms) * 32)), 256, 0,
+                               st>>>(num_ue, num_paths, num_sinusoids, tab, dtau, dpw, first_index, count,
+                                     reinterpret_cast<float2*>(gains_out));
+    e = cudaGetLastError();
+    // the scratch is freed once the stream has consumed it
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    cleanup();
+    if (e != cudaSuccess) return cuda_fail(e, "synthesis launch");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "synthesis");
     return TT_OK;
 }
 

@@ -549,22 +549,21 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
-            return;
-        }
-        for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
-            const SuperInfo si = super_info(p, su);
-            for (int32_t k = 0; k < si.kcount; ++k, ++it) {
-                const int s = it % p.stages;
-                const int kk = it / p.stages;
-                mbar_wait(&full[s], kk & 1);
-                const TileInfo ti = tile_info<R>(p, si.c_first + k, si.tl);
-                // the chunk's sum goes straight into the group row, or into its partial row
-                float2* aggdst = (GEN && p.agg)
-                                     ? p.agg + (static_cast<int64_t>(si.g) * p.nchunks + si.q) * p.n + ti.i0
-                                     : nullptr;
-                consume_tile<R, NOISE, GEN>(p, ti, stage(s), warp, lane, k == 0, aggdst);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+        } else {
+            for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
+                const SuperInfo si = super_info(p, su);
+                for (int32_t k = 0; k < si.kcount; ++k, ++it) {
+                    const int s = it % p.stages;
+                    const int kk = it / p.stages;
+                    mbar_wait(&full[s], kk & 1);
+                    const TileInfo ti = tile_info<R>(p, si.c_first + k, si.tl);
+                    // the chunk's sum goes straight into the group row, or into its partial row
+                    float2* aggdst =
+                        p.agg ? p.agg + (static_cast<int64_t>(si.g) * p.nchunks + si.q) * p.n + ti.i0 : nullptr;
+                    consume_tile<R, NOISE, true>(p, ti, stage(s), warp, lane, k == 0, aggdst);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+                }
             }
         }
     }

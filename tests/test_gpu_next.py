@@ -181,3 +181,52 @@ def test_sparse_n_equal_L_is_dense_and_generic_path(cuda_device, monkeypatch):
     monkeypatch.setenv("TT_KERNEL", "generic")
     assert np.array_equal(_run_sparse(run, cuda_device, 17, [run.N]), sp)
     monkeypatch.delenv("TT_KERNEL")
+
+
+@pytest.mark.parametrize("nu,M", [(0.0, 16), (4e-4, 32), (0.05, 32)])
+def test_jakes_synthesis_parity(cuda_device, nu, M):
+    """f3: GPU-synthesised snapshots vs the oracle's double-precision Jakes
+    (same Philox draws) — relative RMS <= 1e-5 per channel; grid delays identical;
+    windows of a long run (large k) keep the accuracy."""
+    import torch
+
+    from paper_2601_08217_b200 import synth_jakes
+
+    rng = np.random.default_rng(4)
+    C, P = 6, 12
+    tau = np.sort(rng.uniform(0, 300, (C, P)), axis=1).astype(np.float32)
+    tau[:, 0] = 0.0
+    pw = rng.uniform(0.1, 1.0, (C, P)).astype(np.float32)
+    pw /= pw.sum(axis=1, keepdims=True)
+    for k0, K in ((0, 300), (1_000_000, 50)):
+        d, g = synth_jakes(tau, pw, M, nu, seed=99, first_index=k0, count=K, channel_offset=3, device=cuda_device)
+        dr, gr = oracle.synth_jakes(tau, pw, M, nu, 99, k0, K, c_offset=3)
+        assert np.array_equal(d, dr)
+        gg = to_c(g.cpu().numpy())
+        gref = to_c(gr)
+        for c in range(C):
+            err = np.linalg.norm(gg[c] - gref[c]) / np.linalg.norm(gref[c])
+            assert err <= 1e-5, (c, k0, err)
+
+
+def test_synthesised_channel_end_to_end(cuda_device):
+    """f3 feeding the path: synthesise, load, apply; output vs the oracle convolution
+    of the oracle-synthesised snapshots (both tolerances compose)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel, synth_jakes
+
+    rng = np.random.default_rng(8)
+    C, P, S, N = 4, 10, 256, 20_000
+    K = (N - 1) // S + 2
+    tau = np.sort(rng.uniform(0, 500, (C, P)), axis=1).astype(np.float32)
+    pw = np.exp(-3 * tau / 500).astype(np.float32)
+    pw /= pw.sum(axis=1, keepdims=True)
+    d, g = synth_jakes(tau, pw, 32, 0.01, seed=5, first_index=0, count=K, device=cuda_device)
+    dr, gr = oracle.synth_jakes(tau, pw, 32, 0.01, 5, 0, K)
+    x = ttsynth.iq(ttsynth.get("c4").scaled(ues=C, dirs=1, n_per_call=N), 0, C, 0)
+    with Channel(d, S, seed=1, snapshot_capacity=K, device=cuda_device) as ch:
+        ch.load_snapshots(g, 0)
+        y = ch.apply(torch.from_numpy(x).to(cuda_device)).cpu().numpy()
+    ref = oracle.convolve(dr, S, gr, 0, x, 0, 0, N)
+    compare(y, ref, "synthesised channel")

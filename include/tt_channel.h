@@ -183,8 +183,10 @@ tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out
  *   the path's gain is split onto grid taps 2p, 2p+1 at delays floor(tau), floor(tau)+1
  *   with weights (1 - frac, frac) (so the handle has L = 2 num_paths taps).
  * path_delay, path_power: host float [C][P]. delays_out: host int32 [C][2P] receives
- * the grid delays (may be NULL). gains_out: device float [C][count][2P][2].
- * Synchronises `stream` (temporary device tables are freed before returning).
+ * the grid delays (may be NULL). gains_out: device float [C][count][2P][2]. Enqueued on
+ * `stream` (path_delay / path_power are copied before returning); uses a per-device
+ * scratch the library keeps and grows on demand (not thread-safe across devices' calls
+ * beyond an internal lock).
  * Errors: INVALID_ARG (NULL inputs, sizes, nu outside [0, 0.5), delays or powers out of
  * range), OUT_OF_MEMORY, CUDA. */
 tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32_t num_ue, int32_t num_paths,

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 #include <vector>
 
@@ -82,6 +84,13 @@ size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, bool noise, bo
     (void)noise;  // the noise variant needs no extra shared memory (fused epilogue)
     return 128 + static_cast<size_t>(stages) * st;
 }
+
+// device scratch of tt_synth_jakes (one per device, reused across calls)
+struct SynthScratch {
+    unsigned char* buf = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;
+};
 
 }  // namespace
 
@@ -784,27 +793,35 @@ tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32
         }
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    float *dtau = nullptr, *dpw = nullptr;
-    double2* tab = nullptr;
-    const size_t tab_b = static_cast<size_t>(CP) * num_sinusoids * sizeof(double2);
-    auto cleanup = [&]() {
-        cudaFree(dtau);
-        cudaFree(dpw);
-        cudaFree(tab);
-    };
-    cudaError_t e;
-    if ((e = cudaMalloc(&dtau, CP * sizeof(float))) != cudaSuccess ||
-        (e = cudaMalloc(&dpw, CP * sizeof(float))) != cudaSuccess || (e = cudaMalloc(&tab, tab_b)) != cudaSuccess) {
-        cleanup();
-        return cuda_fail(e, "cudaMalloc(synthesis)");
-    }
-    if ((e = cudaMemcpyAsync(dtau, path_delay, CP * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dpw, path_power, CP * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess) {
-        cleanup();
-        return cuda_fail(e, "copy paths");
-    }
     int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
+    TT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    // per-device scratch (path table, delays, powers), kept across calls and grown on
+    // demand; calls on one device are serialised by the lock and by `stream` ordering
+    // (the next call's copies are ordered after this call's kernels via the event)
+    static std::mutex mu;
+    static std::map<int, SynthScratch> scratch;
+    std::lock_guard<std::mutex> lk(mu);
+    SynthScratch& sc = scratch[dev];
+    const size_t need = static_cast<size_t>(CP) * (2 * sizeof(float) + num_sinusoids * sizeof(double2)) + 256;
+    if (need > sc.bytes) {
+        if (sc.buf) {
+            TT_CUDA(cudaDeviceSynchronize(), "synthesis scratch drain");
+            cudaFree(sc.buf);
+            sc.buf = nullptr;
+            sc.bytes = 0;
+        }
+        TT_CUDA(cudaMalloc(&sc.buf, need), "cudaMalloc(synthesis scratch)");
+        sc.bytes = need;
+    }
+    if (!sc.done) TT_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming), "event create");
+    TT_CUDA(cudaStreamWaitEvent(st, sc.done, 0), "stream wait");  // previous users of the scratch
+    double2* tab = reinterpret_cast<double2*>(sc.buf);
+    float* dtau = reinterpret_cast<float*>(sc.buf + static_cast<size_t>(CP) * num_sinusoids * sizeof(double2));
+    float* dpw = dtau + CP;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(dtau, path_delay, CP * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dpw, path_power, CP * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "copy paths");
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tt = CP * num_sinusoids;
     tt::tt_synth_table_kernel<<<static_cast<unsigned>(std::min<int64_t>((tt + 255) / 256, int64_t(sms) * 16)), 256, 0,
@@ -814,12 +831,8 @@ tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32
     tt::tt_synth_gain_kernel<<<static_cast<unsigned>(std::min<int64_t>((tg + 255) / 256, int64_t(sms) * 32)), 256, 0,
                                st>>>(num_ue, num_paths, num_sinusoids, tab, dtau, dpw, first_index, count,
                                      reinterpret_cast<float2*>(gains_out));
-    e = cudaGetLastError();
-    // the scratch is freed once the stream has consumed it
-    cudaError_t e2 = cudaStreamSynchronize(st);
-    cleanup();
-    if (e != cudaSuccess) return cuda_fail(e, "synthesis launch");
-    if (e2 != cudaSuccess) return cuda_fail(e2, "synthesis");
+    TT_CUDA(cudaGetLastError(), "synthesis launch");
+    TT_CUDA(cudaEventRecord(sc.done, st), "event record");
     return TT_OK;
 }
 

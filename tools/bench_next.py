@@ -1,0 +1,204 @@
+#!/usr/bin/env python
+"""Measurement of the NEXT rows on one GPU, one JSON line each.
+
+    python tools/bench_next.py [--steps K] [--warmup W] [--modes aggregate,sparse,links,synth]
+
+Workloads (synthetic, built from BASELINE c4: 122.88 Msps, 0.5 ms slots of 61,440
+samples, 48 taps in [0, 1024], S = 256):
+  aggregate (f1)  the 512 UL channels of c4 summed into one cell per slot
+                  (tt_channel_apply_aggregate, G = 512, per-channel outputs not stored)
+  sparse    (f2)  c4 (1024 channels, 10 dB) with the top-20 taps per interval
+                  ("over 20 channel taps")
+  links     (f4)  512 UEs x 3 gNBs = 1536 links reading 3 shared gNB streams, summed per
+                  UE (tt_channel_set_input_map + aggregate, G = 3)
+  synth     (f3)  Jakes synthesis of one slot's snapshots for c4's 1024 channels
+                  (24 paths -> 48 grid taps, M = 32 sinusoids, 240 snapshots per slot)
+Device-timed with CUDA events over K steps after W warm-up steps; inputs resident.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+import ttsynth  # noqa: E402
+
+
+def timed(fn, steps, warmup, stream):
+    import torch
+
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with bench.ClockSampler(0) as clk:
+        ev[0].record(stream)
+        for i in range(steps):
+            fn(warmup + i)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[-1]), per, clk.summary()
+
+
+def line(mode, metric, value, unit, steps, warmup, ms, per, clk, config, extra=None):
+    d = {"mode": mode, "metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": steps,
+         "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+         "config": config, "call_ms": {"p50": statistics.median(per), "p99": float(np.percentile(per, 99))},
+         "clocks": clk}
+    if extra:
+        d.update(extra)
+    print(json.dumps(d), flush=True)
+
+
+def fp32_peak(peaks):
+    return bench.SM_COUNT_NOMINAL * bench.FP32_LANES_PER_SM * 2 * peaks["sm_max_mhz"] * 1e6
+
+
+def run_aggregate(args, dev, peaks):
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    w = ttsynth.get("c4").scaled(dirs=1)  # the 512 UL channels
+    C, n = w.C, w.n_per_call
+    steps_total = args.warmup + args.steps + 1
+    K = (steps_total * n - 1) // w.S + 2
+    P = min(steps_total, max(2, math.ceil(4 * bench.L2_BYTES / (C * n * 8))))
+    xs = [ttsynth.iq(w, 0, C, i, backend="torch", device=dev) for i in range(P)]
+    agg = torch.empty((1, n, 2), dtype=torch.float32, device=dev)
+    ch = Channel(ttsynth.delays(w), w.S, seed=1, snapshot_capacity=K, device=dev)
+    ch.load_snapshots(ttsynth.snapshots(w, 0, C, K, backend="torch", device=dev), 0)
+    torch.cuda.synchronize()
+    el, per, clk = timed(lambda i: ch.apply_aggregate(xs[i % P], C, agg=agg, noise_sigma=w.sigma), args.steps,
+                         args.warmup, torch.cuda.current_stream())
+    ch.close()
+    ms = el / args.steps
+    sps = C * n / (ms / 1e3)
+    ach = 8.0 * w.L * sps / 1e12
+    line("aggregate", "UL channel samples convolved and summed per s (one cell)", sps, "samples/s", args.steps,
+         args.warmup, ms, per, clk,
+         {"workload": "c4 UL: 512 UL channels -> 1 cell aggregate per 0.5 ms slot (NEXT f1)", "channels": C,
+          "group": C, "samples_per_call": n, "taps": w.L, "snapshot_period": w.S, "snr_db": w.snr_db},
+         {"roofline": {"bound": "alu", "achieved": ach, "peak": fp32_peak(peaks) / 1e12, "unit": "TFLOP/s",
+                       "frac": ach / (fp32_peak(peaks) / 1e12)},
+          "realtime_ues": int(sps // w.rate_sps)})
+
+
+def run_sparse(args, dev, peaks, top_n=20):
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    w = ttsynth.get("c4")
+    C, n = w.C, w.n_per_call
+    steps_total = args.warmup + args.steps + 1
+    K = (steps_total * n - 1) // w.S + 2
+    P = min(steps_total, max(2, math.ceil(4 * bench.L2_BYTES / (C * n * 8))))
+    xs = [ttsynth.iq(w, 0, C, i, backend="torch", device=dev) for i in range(P)]
+    y = torch.empty_like(xs[0])
+    ch = Channel(ttsynth.delays(w), w.S, seed=1, snapshot_capacity=K, device=dev)
+    ch.set_top_n(top_n)
+    ch.load_snapshots(ttsynth.snapshots(w, 0, C, K, backend="torch", device=dev), 0)
+    torch.cuda.synchronize()
+    el, per, clk = timed(lambda i: ch.apply(xs[i % P], out=y, noise_sigma=w.sigma), args.steps, args.warmup,
+                         torch.cuda.current_stream())
+    ch.close()
+    ms = el / args.steps
+    sps = C * n / (ms / 1e3)
+    ach = 8.0 * top_n * sps / 1e12
+    line("sparse", "channel-convolved complex samples/s, top-%d taps" % top_n, sps, "samples/s", args.steps,
+         args.warmup, ms, per, clk,
+         {"workload": "c4 with the top-%d of 48 taps per snapshot interval (NEXT f2)" % top_n, "channels": C,
+          "samples_per_call": n, "taps": w.L, "top_n": top_n, "snapshot_period": w.S, "snr_db": w.snr_db},
+         {"roofline": {"bound": "alu", "achieved": ach, "peak": fp32_peak(peaks) / 1e12, "unit": "TFLOP/s",
+                       "frac": ach / (fp32_peak(peaks) / 1e12), "flops_per_sample": 8 * top_n},
+          "realtime_ues": w.realtime_ues(sps)})
+
+
+def run_links(args, dev, peaks, B=3):
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    base = ttsynth.get("c4")
+    w = base.scaled(ues=base.ues * B, dirs=1)  # link (u, b) = channel u*B + b
+    C, n = w.C, w.n_per_call
+    steps_total = args.warmup + args.steps + 1
+    K = (steps_total * n - 1) // w.S + 2
+    xs = [ttsynth.iq(w, 0, B, i, backend="torch", device=dev) for i in range(4)]  # the gNB streams
+    agg = torch.empty((base.ues, n, 2), dtype=torch.float32, device=dev)
+    ch = Channel(ttsynth.delays(w), w.S, seed=1, snapshot_capacity=K, device=dev)
+    ch.set_input_map(np.tile(np.arange(B, dtype=np.int32), base.ues), B)
+    ch.load_snapshots(ttsynth.snapshots(w, 0, C, K, backend="torch", device=dev), 0)
+    torch.cuda.synchronize()
+    el, per, clk = timed(lambda i: ch.apply_aggregate(xs[i % 4], B, agg=agg, noise_sigma=w.sigma), args.steps,
+                         args.warmup, torch.cuda.current_stream())
+    ch.close()
+    ms = el / args.steps
+    sps = C * n / (ms / 1e3)
+    ach = 8.0 * w.L * sps / 1e12
+    line("links", "link samples convolved per s (UE received sums over B gNBs)", sps, "samples/s", args.steps,
+         args.warmup, ms, per, clk,
+         {"workload": "512 UEs x %d gNBs: 1536 links from 3 shared gNB streams, summed per UE (NEXT f4)" % B,
+          "links": C, "gnbs": B, "samples_per_call": n, "taps": w.L, "snapshot_period": w.S},
+         {"roofline": {"bound": "alu", "achieved": ach, "peak": fp32_peak(peaks) / 1e12, "unit": "TFLOP/s",
+                       "frac": ach / (fp32_peak(peaks) / 1e12)},
+          "realtime_ues": int((sps / B) // w.rate_sps)})
+
+
+def run_synth(args, dev, peaks, P=24, M=32):
+    import torch
+
+    from paper_2601_08217_b200 import synth_jakes
+
+    w = ttsynth.get("c4")
+    C = w.C
+    per_slot = w.n_per_call // w.S  # snapshots per 0.5 ms slot
+    rng = np.random.default_rng(0)
+    tau = np.sort(rng.uniform(0, 1023, (C, P)), axis=1).astype(np.float32)
+    pw = np.exp(-3 * tau / 1024).astype(np.float32)
+    pw /= pw.sum(axis=1, keepdims=True)
+    nu = 194.4 * w.S / w.rate_sps  # 60 km/h at 3.5 GHz
+
+    def step(i):
+        synth_jakes(tau, pw, M, nu, seed=3, first_index=i * per_slot, count=per_slot, device=dev)
+
+    el, per, clk = timed(step, args.steps, args.warmup, torch.cuda.current_stream())
+    ms = el / args.steps
+    terms = C * P * per_slot * M
+    line("synth", "Jakes path-snapshots synthesised per s", C * P * per_slot / (ms / 1e3), "path-snapshots/s",
+         args.steps, args.warmup, ms, per, clk,
+         {"workload": "c4 channels x 24 paths x 240 snapshots per slot, M=32, f_D=194.4 Hz (NEXT f3)",
+          "channels": C, "paths": P, "sinusoids": M, "snapshots_per_step": per_slot, "nu": nu},
+         {"sinusoid_terms_per_s": terms / (ms / 1e3),
+          "note": "includes host path validation, table build and a stream sync per call"})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--modes", default="aggregate,sparse,links,synth")
+    args = ap.parse_args()
+    import torch
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    peaks = bench._peaks()
+    for m in args.modes.split(","):
+        {"aggregate": run_aggregate, "sparse": run_sparse, "links": run_links, "synth": run_synth}[m](args, dev, peaks)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -59,6 +59,7 @@ struct DeviceGuard {
 // one plan per noise flag (they may differ in R if the variants' budgets ever differ).
 struct TiledPlan {
     int R = 0;           // outputs per consumer thread (0: does not fit -> generic kernel)
+    int CW = 16;         // consumer warps (tile T = CW x 32 x R)
     int stages = 2;      // shared-memory pipeline depth (2..4)
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;      // gain rows staged per tile
@@ -75,8 +76,8 @@ constexpr size_t kSmemBudget = 227 * 1024;  // one CTA per SM
 
 // must match tt_conv_kernel's layout: 128 B of barriers + `stages` x [win | coef | xo]
 // (L = taps per gain row: top-n when sparse, whose offsets come one row per interval)
-size_t smem_bytes(int R, int stages, int H, int L, int L4, int S, bool noise, bool xo_rows, int* nk_out) {
-    const int T = tt::kConsumerWarps * 32 * R;
+size_t smem_bytes(int R, int CW, int stages, int H, int L, int L4, int S, bool noise, bool xo_rows, int* nk_out) {
+    const int T = CW * 32 * R;
     const int nk = (T - 1) / S + 2;  // worst-case intervals touched by a tile
     *nk_out = nk;
     const size_t st = (static_cast<size_t>(H) + T) * 8 + static_cast<size_t>(nk) * L * 16 +
@@ -129,14 +130,20 @@ struct tt_channel_s {
 
 namespace {
 
-template <int R, bool NOISE>
+template <int R, int CW, bool NOISE>
 cudaError_t prepare_kernel(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(tt::tt_conv_kernel<R, NOISE, false>,
+    cudaError_t e = cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(tt::tt_conv_kernel<R, NOISE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem));
 }
+
+// tile shapes (R outputs per thread, CW consumer warps), in order of preference
+struct Shape {
+    int R, CW;
+};
+constexpr Shape kShapes[] = {{8, 16}, {16, 8}, {4, 16}, {2, 16}};
 
 template <bool NOISE>
 cudaError_t prepare_tiled(tt_channel_s* h) {
@@ -147,31 +154,30 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     const int max_stages = fs ? std::max(2, std::min(tt::kMaxStages, atoi(fs))) : tt::kMaxStages;
     const bool sparse = h->top_n > 0;
     const int Lr = sparse ? h->top_n : h->L, L4r = sparse ? h->n4 : h->L4;
-    // the largest R that fits; with a power-of-two S >= 32 a warp's rows read one
-    // broadcast gain row per snapshot interval they cover (tt_conv.cuh taps_grouped)
-    const int Rs[3] = {8, 4, 2};
-    const bool pow2 = (h->S & (h->S - 1)) == 0 && h->S >= 32;
-    int pick = -1;
-    for (int pass = 0; pass < 2 && pick < 0; ++pass) {
-        for (int i = 0; i < 3; ++i) {
-            int nk = 0;
-            if (smem_bytes(Rs[i], 2, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget) continue;
-            if (pass == 0 && !pow2) continue;
-            int stages = max_stages;
-            while (stages > 2 && smem_bytes(Rs[i], stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget)
-                --stages;
-            pick = i;
-            tp.R = Rs[i];
-            tp.stages = stages;
-            tp.smem = smem_bytes(Rs[i], stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk);
-            tp.nk_max = nk;
-            break;
-        }
+    // TT_TILE=RxCW (experiments) restricts the shape
+    int fR = 0, fCW = 0;
+    if (const char* ft = getenv("TT_TILE")) sscanf(ft, "%dx%d", &fR, &fCW);
+    // the first shape that fits with >= 2 stages; (16, 8) only when forced (measured
+    // slower at the BASELINE configs)
+    for (const Shape& sh : kShapes) {
+        if (fR ? (sh.R != fR || sh.CW != fCW) : (sh.CW != 16)) continue;
+        int nk = 0;
+        if (smem_bytes(sh.R, sh.CW, 2, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget) continue;
+        int stages = max_stages;
+        while (stages > 2 && smem_bytes(sh.R, sh.CW, stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget)
+            --stages;
+        tp.R = sh.R;
+        tp.CW = sh.CW;
+        tp.stages = stages;
+        tp.smem = smem_bytes(sh.R, sh.CW, stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk);
+        tp.nk_max = nk;
+        break;
     }
-    switch (tp.R) {
-        case 8: return prepare_kernel<8, NOISE>(tp.smem);
-        case 4: return prepare_kernel<4, NOISE>(tp.smem);
-        case 2: return prepare_kernel<2, NOISE>(tp.smem);
+    switch (tp.R * 100 + tp.CW) {
+        case 816: return prepare_kernel<8, 16, NOISE>(tp.smem);
+        case 1608: return prepare_kernel<16, 8, NOISE>(tp.smem);
+        case 416: return prepare_kernel<4, 16, NOISE>(tp.smem);
+        case 216: return prepare_kernel<2, 16, NOISE>(tp.smem);
         default: return cudaSuccess;  // generic kernel
     }
 }
@@ -308,7 +314,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     } else if (h->plan.tiled[noise ? 1 : 0].R != 0 &&
                (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row || sparse)) {
         const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
-        const int T = tt::kConsumerWarps * 32 * tp.R;
+        const int T = tp.CW * 32 * tp.R;
         p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
         if (ar.agg) {
@@ -327,25 +333,27 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         if (p.total_super >= (int64_t(1) << 31) || p.total_tiles >= (int64_t(1) << 31))
             return fail(TT_ERR_INVALID_ARG, "call too large: %lld work items", (long long)p.total_super);
         const int64_t grid = std::min<int64_t>(p.total_super, static_cast<int64_t>(h->num_sms));
-        const dim3 g(static_cast<unsigned>(grid));
+        const dim3 g(static_cast<unsigned>(grid)), b((tp.CW + 1) * 32);
         const size_t sm = tp.smem;
-        const unsigned b0 = tt::kThreads, b1 = tt::kThreads;
         // the general variant only when a group sum or sparse offsets are in play
         const bool gen = ar.agg || sparse;
-        switch (tp.R * 4 + (noise ? 2 : 0) + (gen ? 1 : 0)) {
-            case 32: tt::tt_conv_kernel<8, false, false><<<g, b0, sm, st>>>(p); break;
-            case 33: tt::tt_conv_kernel<8, false, true><<<g, b0, sm, st>>>(p); break;
-            case 34: tt::tt_conv_kernel<8, true, false><<<g, b1, sm, st>>>(p); break;
-            case 35: tt::tt_conv_kernel<8, true, true><<<g, b1, sm, st>>>(p); break;
-            case 16: tt::tt_conv_kernel<4, false, false><<<g, b0, sm, st>>>(p); break;
-            case 17: tt::tt_conv_kernel<4, false, true><<<g, b0, sm, st>>>(p); break;
-            case 18: tt::tt_conv_kernel<4, true, false><<<g, b1, sm, st>>>(p); break;
-            case 19: tt::tt_conv_kernel<4, true, true><<<g, b1, sm, st>>>(p); break;
-            case 8: tt::tt_conv_kernel<2, false, false><<<g, b0, sm, st>>>(p); break;
-            case 9: tt::tt_conv_kernel<2, false, true><<<g, b0, sm, st>>>(p); break;
-            case 10: tt::tt_conv_kernel<2, true, false><<<g, b1, sm, st>>>(p); break;
-            default: tt::tt_conv_kernel<2, true, true><<<g, b1, sm, st>>>(p); break;
+#define TT_LAUNCH(RR, CC)                                                                 \
+    do {                                                                                  \
+        if (noise) {                                                                      \
+            if (gen) tt::tt_conv_kernel<RR, CC, true, true><<<g, b, sm, st>>>(p);         \
+            else tt::tt_conv_kernel<RR, CC, true, false><<<g, b, sm, st>>>(p);            \
+        } else {                                                                          \
+            if (gen) tt::tt_conv_kernel<RR, CC, false, true><<<g, b, sm, st>>>(p);        \
+            else tt::tt_conv_kernel<RR, CC, false, false><<<g, b, sm, st>>>(p);           \
+        }                                                                                 \
+    } while (0)
+        switch (tp.R * 100 + tp.CW) {
+            case 816: TT_LAUNCH(8, 16); break;
+            case 1608: TT_LAUNCH(16, 8); break;
+            case 416: TT_LAUNCH(4, 16); break;
+            default: TT_LAUNCH(2, 16); break;
         }
+#undef TT_LAUNCH
         if (ar.agg && nchunks > 1) {
             const int64_t tot = static_cast<int64_t>(ngroups) * n;
             const int64_t gg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);

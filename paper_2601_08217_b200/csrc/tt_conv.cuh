@@ -38,7 +38,7 @@
 
 namespace tt {
 
-constexpr int kConsumerWarps = 16;
+constexpr int kConsumerWarps = 16;                   // default tile shape: 16 consumer warps
 constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
 constexpr int kMaxStages = 4;
 
@@ -190,9 +190,9 @@ __device__ __forceinline__ SuperInfo super_info(const ConvParams& p, int64_t su6
     return si;
 }
 
-template <int R>
+template <int R, int CW>
 __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int32_t c, int32_t tl) {
-    constexpr int T = kConsumerWarps * 32 * R;
+    constexpr int T = CW * 32 * R;
     TileInfo ti;
     ti.c = c;
     ti.i0 = static_cast<int64_t>(tl) * T;
@@ -335,7 +335,7 @@ __device__ __forceinline__ void taps_grouped_rt(const ConvParams& p, const float
 
 // Consumer warp: the 32R outputs of warp `cw` in tile `ti`. GEN: the general variant
 // (group sums, sparse per-interval offsets); the plain variant compiles none of it.
-template <int R, bool NOISE, bool GEN>
+template <int R, int CW, bool NOISE, bool GEN>
 __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
                                              int lane, bool first, float2* aggdst) {
     const int32_t obase = cw * 32 * R + lane;
@@ -478,13 +478,14 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
     // window index of call-local sample n - H + i is Tt + i
     if (ti.i0 + ti.Tt == p.n) {
         float2* hw = p.hist_wr + static_cast<int64_t>(ti.c) * p.H;
-        for (int32_t i = cw * 32 + lane; i < p.H; i += kConsumerWarps * 32) hw[i] = st.win[ti.Tt + i];
+        for (int32_t i = cw * 32 + lane; i < p.H; i += CW * 32) hw[i] = st.win[ti.Tt + i];
     }
 }
 
-template <int R, bool NOISE, bool GEN>
-__global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p) {
-    constexpr int T = kConsumerWarps * 32 * R;
+// CW consumer warps + 1 producer warp; tile T = CW x 32 x R outputs of one channel
+template <int R, int CW, bool NOISE, bool GEN>
+__global__ void __launch_bounds__((CW + 1) * 32, 1) tt_conv_kernel(const ConvParams p) {
+    constexpr int T = CW * 32 * R;
     extern __shared__ __align__(128) unsigned char smem[];
     // layout: [full kMaxStages x 8 B | empty kMaxStages x 8 B | pad to 128][stage 0][stage 1]...
     //   stage = [win (H+T) float2][coef nk_max x L float4][xo (sparse: nk_max x) L4 int32]
@@ -505,13 +506,13 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], CW);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (warp == kConsumerWarps) {
+    if (warp == CW) {
         // producer: run ahead of the consumers by up to `stages` tiles
         int it = 0;
         if constexpr (!GEN) {
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
                 if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
                 const uint32_t cl = static_cast<uint32_t>(w) / static_cast<uint32_t>(p.tiles_per_ch);
                 const int32_t tl = static_cast<int32_t>(static_cast<uint32_t>(w) - cl * p.tiles_per_ch);
-                produce_tile<R>(p, tile_info<R>(p, p.c_lo + static_cast<int32_t>(cl), tl), stage(s), &full[s], lane);
+                produce_tile<R>(p, tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(cl), tl), stage(s), &full[s], lane);
             }
         } else {
             for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
                     const int s = it % p.stages;
                     const int kk = it / p.stages;
                     if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
-                    produce_tile<R>(p, tile_info<R>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
+                    produce_tile<R>(p, tile_info<R, CW>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
                 }
             }
         }
@@ -544,8 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
                 mbar_wait(&full[s], kk & 1);
                 const uint32_t cl = static_cast<uint32_t>(w) / static_cast<uint32_t>(p.tiles_per_ch);
                 const int32_t tl = static_cast<int32_t>(static_cast<uint32_t>(w) - cl * p.tiles_per_ch);
-                const TileInfo ti = tile_info<R>(p, p.c_lo + static_cast<int32_t>(cl), tl);
-                consume_tile<R, NOISE, false>(p, ti, stage(s), warp, lane, true, nullptr);
+                const TileInfo ti = tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(cl), tl);
+                consume_tile<R, CW, NOISE, false>(p, ti, stage(s), warp, lane, true, nullptr);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
@@ -556,11 +557,11 @@ __global__ void __launch_bounds__(kThreads, 1) tt_conv_kernel(const ConvParams p
                     const int s = it % p.stages;
                     const int kk = it / p.stages;
                     mbar_wait(&full[s], kk & 1);
-                    const TileInfo ti = tile_info<R>(p, si.c_first + k, si.tl);
+                    const TileInfo ti = tile_info<R, CW>(p, si.c_first + k, si.tl);
                     // the chunk's sum goes straight into the group row, or into its partial row
                     float2* aggdst =
                         p.agg ? p.agg + (static_cast<int64_t>(si.g) * p.nchunks + si.q) * p.n + ti.i0 : nullptr;
-                    consume_tile<R, NOISE, true>(p, ti, stage(s), warp, lane, k == 0, aggdst);
+                    consume_tile<R, CW, NOISE, true>(p, ti, stage(s), warp, lane, k == 0, aggdst);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                 }

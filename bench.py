@@ -232,7 +232,6 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sigma", type=float, default=None, help="override the config's noise sigma (experiments)")
-    ap.add_argument("--no-lookahead", action="store_true", help="generate all noise inside the kernel (experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -275,8 +274,6 @@ def main():
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     sigma = w.sigma if args.sigma is None else args.sigma
-    if sigma > 0 and not one_shot and not args.no_lookahead:
-        ch.set_noise_lookahead(n)  # streaming slots: next slot's AWGN generated alongside this slot
 
     # ---- device-resident timed region ----------------------------------------------
     def step(xin):

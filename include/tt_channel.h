@@ -135,17 +135,6 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
 tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                            tt_stream_t stream);
 
-/* Noise lookahead (a performance option for streaming slots; NS "optional AWGN"): the
- * AWGN of a call does not depend on x, so after each tt_channel_apply with sigma > 0 the
- * library generates w for the predicted next call — same n, starting where this one
- * ended, same sigma — on an internal stream, concurrently with the convolution it just
- * enqueued. If the next call matches, its kernel adds the precomputed w instead of
- * generating it (identical values, docs/tt-normal-v1.md); otherwise it generates as
- * usual. max_samples: the largest per-channel call size to cover (0 = off, the
- * default); allocates 2 x C x max_samples x 8 B. Synchronises the device.
- * Errors: INVALID_ARG (NULL handle, max_samples < 0), OUT_OF_MEMORY, CUDA. */
-tt_status tt_channel_set_noise_lookahead(tt_channel_t h, int64_t max_samples);
-
 /* NEXT f2 (§III-C "convolution is performed only with the top-n dominant taps at
  * each time step"): from now on each snapshot interval k sums only its top_n taps of
  * largest |g_{l,k}|^2 (float32 fl(re*re) + fl(im*im); ties to the smaller delay, then

@@ -31,7 +31,6 @@ EXPORTS = (
     "tt_channel_load_snapshots",
     "tt_channel_apply",
     "tt_channel_apply_host",
-    "tt_channel_set_noise_lookahead",
     "tt_channel_set_top_n",
     "tt_channel_set_input_map",
     "tt_channel_apply_aggregate",
@@ -95,7 +94,6 @@ def lib() -> ct.CDLL:
             L.tt_channel_apply.argtypes = [P, P, P, i64, f32, P]
             L.tt_channel_apply_host.argtypes = [P, P, P, i64, f32, P]
             L.tt_channel_set_top_n.argtypes = [P, i32]
-            L.tt_channel_set_noise_lookahead.argtypes = [P, i64]
             L.tt_channel_set_input_map.argtypes = [P, P, i32]
             L.tt_channel_apply_aggregate.argtypes = [P, P, P, P, i32, i64, f32, P]
             L.tt_synth_jakes.argtypes = [P, P, i32, i32, i32, ct.c_double, u64, i64, i64, i64, P, P, P]
@@ -104,8 +102,7 @@ def lib() -> ct.CDLL:
             L.tt_channel_get_info.argtypes = [P, ct.POINTER(ChannelInfo)]
             L.tt_channel_destroy.argtypes = [P]
             for f in ("tt_channel_create", "tt_channel_load_snapshots", "tt_channel_apply", "tt_channel_apply_host",
-                      "tt_channel_set_noise_lookahead",
-    "tt_channel_set_top_n",
+                      "tt_channel_set_top_n",
     "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset",
                       "tt_channel_get_info", "tt_channel_destroy"):
                 getattr(L, f).restype = ct.c_int
@@ -143,10 +140,6 @@ def tt_channel_apply(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_si
 def tt_channel_apply_host(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_sigma: float,
                           stream: int) -> None:
     check(lib().tt_channel_apply_host(h, in_ptr, out_ptr, n_samples, noise_sigma, stream))
-
-
-def tt_channel_set_noise_lookahead(h: int, max_samples: int) -> None:
-    check(lib().tt_channel_set_noise_lookahead(h, max_samples))
 
 
 def tt_channel_set_top_n(h: int, top_n: int) -> None:

@@ -105,10 +105,6 @@ class Channel:
                               _stream_ptr(stream))
         return out
 
-    def set_noise_lookahead(self, max_samples: int) -> None:
-        """Generate the next streaming call's AWGN concurrently with this call (0 = off)."""
-        _lib.tt_channel_set_noise_lookahead(self.handle, int(max_samples))
-
     def set_top_n(self, top_n: int) -> None:
         """NEXT f2: sum only the top_n dominant taps per snapshot interval (0 = dense)."""
         _lib.tt_channel_set_top_n(self.handle, int(top_n))

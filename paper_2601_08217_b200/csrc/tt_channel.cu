@@ -116,15 +116,6 @@ struct tt_channel_s {
     int32_t* soff = nullptr;    // [C][cap][n4] window offsets of the selected taps
     int32_t in_rows = 0;        // rows of `in` when in_row is set
     float2* agg_scratch = nullptr;  // chunk sums / per-channel outputs for tt_channel_apply_aggregate
-    // noise lookahead (tt_channel_set_noise_lookahead): w of the predicted next call
-    int64_t la_cap = 0;             // samples per channel per buffer (0 = off)
-    float2* la_buf[2] = {nullptr, nullptr};
-    cudaStream_t la_side = nullptr;
-    cudaEvent_t la_ready[2] = {}, la_used[2] = {};
-    bool la_valid = false;
-    int la_idx = 0;
-    int64_t la_t = 0, la_n = 0;
-    float la_sigma = 0.f;
     size_t agg_scratch_elems = 0;
     float2* load_stage = nullptr;  // device staging for host-memory snapshot sources
     size_t load_stage_elems = 0;
@@ -243,9 +234,8 @@ struct AggReq {
 };
 
 tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int32_t c_hi, int64_t n, float sigma,
-                 cudaStream_t st, const AggReq& ar = AggReq{}, const float2* wbuf = nullptr) {
+                 cudaStream_t st, const AggReq& ar = AggReq{}) {
     tt::ConvParams p{};
-    p.wbuf = wbuf;
     p.x = x;
     p.y = y;
     p.in_row = h->in_row;
@@ -422,12 +412,6 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->sring);
     cudaFree(h->soff);
     cudaFree(h->agg_scratch);
-    for (int i = 0; i < 2; ++i) {
-        cudaFree(h->la_buf[i]);
-        if (h->la_ready[i]) cudaEventDestroy(h->la_ready[i]);
-        if (h->la_used[i]) cudaEventDestroy(h->la_used[i]);
-    }
-    if (h->la_side) cudaStreamDestroy(h->la_side);
     cudaFree(h->load_stage);
     cudaFree(h->stage);
     for (int i = 0; i < 3; ++i) {
@@ -616,52 +600,14 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
     return TT_OK;
 }
 
-namespace {
-// noise lookahead: generate w for the call after this one, [t + n, t + 2n), into the
-// buffer the next call will read, on the side stream (after the last reader of that
-// buffer finished)
-tt_status lookahead_next(tt_channel_s* h, int64_t t_next, int64_t n, float sigma, int j) {
-    TT_CUDA(cudaStreamWaitEvent(h->la_side, h->la_used[j], 0), "lookahead wait");
-    const float sc = static_cast<float>(static_cast<double>(sigma) * 0x1.6a09e667f3bcdp-1);
-    tt::tt_noise_fill_kernel<<<static_cast<unsigned>(h->num_sms), 128, 0, h->la_side>>>(
-        h->C, t_next, n, static_cast<uint32_t>(h->seed), static_cast<uint32_t>(h->seed >> 32), h->chan_off, 0, sc,
-        h->la_buf[j]);
-    TT_CUDA(cudaGetLastError(), "noise lookahead launch");
-    TT_CUDA(cudaEventRecord(h->la_ready[j], h->la_side), "event record");
-    h->la_valid = true;
-    h->la_idx = j;
-    h->la_t = t_next;
-    h->la_n = n;
-    h->la_sigma = sigma;
-    return TT_OK;
-}
-}  // namespace
-
 tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                            tt_stream_t stream) {
     tt_status s = check_apply(h, in, out, n_samples, noise_sigma);
     if (s != TT_OK) return s;
     DeviceGuard dg(h->dev);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const bool la = h->la_cap > 0 && noise_sigma > 0.0f && n_samples <= h->la_cap &&
-                    h->plan.tiled[1].R != 0 && h->plan.kind != TT_KERNEL_RW;
-    const float2* wbuf = nullptr;
-    if (la && h->la_valid && h->la_t == h->t && h->la_n == n_samples && h->la_sigma == noise_sigma) {
-        TT_CUDA(cudaStreamWaitEvent(st, h->la_ready[h->la_idx], 0), "lookahead wait");
-        wbuf = h->la_buf[h->la_idx];
-    }
     s = launch(h, reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), 0, h->C, n_samples,
-               noise_sigma, st, AggReq{}, wbuf);
+               noise_sigma, static_cast<cudaStream_t>(stream));
     if (s != TT_OK) return s;
-    if (la) {
-        int j = 0;
-        if (wbuf) {
-            TT_CUDA(cudaEventRecord(h->la_used[h->la_idx], st), "event record");
-            j = 1 - h->la_idx;
-        }
-        s = lookahead_next(h, h->t + n_samples, n_samples, noise_sigma, j);
-        if (s != TT_OK) return s;
-    }
     h->t += n_samples;
     if (h->H > 0) h->p ^= 1;
     return TT_OK;
@@ -817,12 +763,6 @@ tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out
         if (h->agg_scratch) {
             TT_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "scratch drain");
             cudaFree(h->agg_scratch);
-    for (int i = 0; i < 2; ++i) {
-        cudaFree(h->la_buf[i]);
-        if (h->la_ready[i]) cudaEventDestroy(h->la_ready[i]);
-        if (h->la_used[i]) cudaEventDestroy(h->la_used[i]);
-    }
-    if (h->la_side) cudaStreamDestroy(h->la_side);
             h->agg_scratch = nullptr;
             h->agg_scratch_elems = 0;
         }
@@ -913,35 +853,6 @@ tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream) {
                 "zero history");
     h->t = 0;
     h->p = 0;
-    h->la_valid = false;
-    return TT_OK;
-}
-
-tt_status tt_channel_set_noise_lookahead(tt_channel_t h, int64_t max_samples) {
-    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
-    if (max_samples < 0) return fail(TT_ERR_INVALID_ARG, "max_samples must be >= 0");
-    DeviceGuard dg(h->dev);
-    if (h->la_side) TT_CUDA(cudaStreamSynchronize(h->la_side), "lookahead drain");
-    TT_CUDA(cudaDeviceSynchronize(), "lookahead drain");
-    for (int i = 0; i < 2; ++i) {
-        cudaFree(h->la_buf[i]);
-        h->la_buf[i] = nullptr;
-    }
-    h->la_cap = 0;
-    h->la_valid = false;
-    if (max_samples == 0) return TT_OK;
-    if (!h->la_side) {
-        TT_CUDA(cudaStreamCreateWithFlags(&h->la_side, cudaStreamNonBlocking), "stream create");
-        for (int i = 0; i < 2; ++i) {
-            TT_CUDA(cudaEventCreateWithFlags(&h->la_ready[i], cudaEventDisableTiming), "event create");
-            TT_CUDA(cudaEventCreateWithFlags(&h->la_used[i], cudaEventDisableTiming), "event create");
-            TT_CUDA(cudaEventRecord(h->la_used[i], h->la_side), "event record");
-        }
-    }
-    for (int i = 0; i < 2; ++i)
-        TT_CUDA(cudaMalloc(&h->la_buf[i], static_cast<size_t>(h->C) * max_samples * sizeof(float2)),
-                "cudaMalloc(noise lookahead)");
-    h->la_cap = max_samples;
     return TT_OK;
 }
 
@@ -961,8 +872,7 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->seed = h->seed;
     info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2) +
                                               h->load_stage_elems * sizeof(float2) +
-                                              h->agg_scratch_elems * sizeof(float2) +
-                                              2 * static_cast<size_t>(h->C) * h->la_cap * sizeof(float2));
+                                              h->agg_scratch_elems * sizeof(float2));
     info->kernel = h->plan.kind;
     info->top_n = h->top_n;
     info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? tt::rw::R
@@ -974,7 +884,6 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
 tt_status tt_channel_destroy(tt_channel_t h) {
     if (!h) return TT_OK;
     DeviceGuard dg(h->dev);
-    if (h->la_side) cudaStreamSynchronize(h->la_side);
     cudaDeviceSynchronize();
     free_all(h);
     delete h;

@@ -69,7 +69,6 @@ struct ConvParams {
     int32_t L, L4, H, S;
     int32_t nk_max;         // max snapshot intervals a tile touches
     int32_t stages;         // shared-memory pipeline depth (<= kMaxStages)
-    const float2* wbuf;     // NOISE: precomputed w [C_launch][n] (noise lookahead), or nullptr = generate
     uint32_t key0, key1;    // noise key
     float noise_sc;         // sigma / sqrt(2) as float; 0 = no noise
     int32_t s_shift;        // log2(S) if S is a power of two, else -1
@@ -416,18 +415,7 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
         float2 out[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) out[r] = make_float2(__fsub_rn(A[r].x, B[r].y), __fadd_rn(A[r].y, B[r].x));
-        if (NOISE && p.wbuf) {
-            // w was generated ahead of time by tt_noise_fill_kernel (identical values)
-            const float2* wr = p.wbuf + static_cast<int64_t>(ti.c - p.c_lo) * p.n + ti.i0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int32_t o = obase + r * 32;
-                if (o < ti.Tt) {
-                    const float2 wv = __ldcs(wr + o);
-                    out[r] = make_float2(__fadd_rn(out[r].x, wv.x), __fadd_rn(out[r].y, wv.y));
-                }
-            }
-        } else if constexpr (NOISE) {
+        if constexpr (NOISE) {
             const int64_t nb = p.t + ti.i0 + obase;  // global sample of row 0
             const uint32_t cg = static_cast<uint32_t>(p.chan_offset + ti.c);
             const bool even_base = ((p.t + ti.i0) & 1) == 0;  // CTA-uniform
@@ -638,30 +626,6 @@ __global__ void tt_history_kernel(const ConvParams p, int32_t nch) {
         const int64_t row = p.in_row ? static_cast<int64_t>(__ldg(p.in_row + c)) : cl;
         p.hist_wr[static_cast<int64_t>(c) * p.H + i] =
             m >= 0 ? p.x[row * p.n + m] : p.hist_rd[static_cast<int64_t>(c) * p.H + (p.H + m)];
-    }
-}
-
-// Noise lookahead (tt_channel_set_noise_lookahead): w_c[t .. t+n) of channels [c_lo,
-// c_lo + C) into w [C][n], generated on a side stream while the previous call's
-// convolution runs — a small grid that fits next to the persistent convolution CTA on
-// each SM and uses the issue slots its shared-memory-bound tap loop leaves free. Same
-// Philox words and transform as the fused epilogue, so the values are identical.
-__global__ void __launch_bounds__(128) tt_noise_fill_kernel(int32_t C, int64_t t, int64_t n, uint32_t key0,
-                                                            uint32_t key1, int64_t chan_offset, int32_t c_lo,
-                                                            float sc, float2* __restrict__ w) {
-    const int64_t m0 = t >> 1;
-    const int64_t npair = ((t + n - 1) >> 1) - m0 + 1;
-    const int64_t tot = static_cast<int64_t>(C) * npair;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t cl = e / npair;
-        const int64_t m = m0 + (e - cl * npair);
-        const u32x4 q = philox4x32_10(static_cast<uint32_t>(m), static_cast<uint32_t>(static_cast<uint64_t>(m) >> 32),
-                                      static_cast<uint32_t>(chan_offset + c_lo + cl), 0u, key0, key1);
-        const int64_t i0 = 2 * m - t;  // call-local index of sample 2m (may be -1)
-        float2* wr = w + cl * n;
-        if (i0 >= 0) wr[i0] = noise_from_words(q.a, q.b, sc);
-        if (i0 + 1 < n) wr[i0 + 1] = noise_from_words(q.c, q.d, sc);
     }
 }
 

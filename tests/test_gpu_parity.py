@@ -187,33 +187,3 @@ def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     assert np.array_equal(outs["rw"], outs["tiled"])
     assert np.array_equal(outs["rw"], outs["generic"])
     compare(outs["rw"], run.oracle(), name)
-
-
-def test_noise_lookahead_bit_identical(cuda_device):
-    """The noise lookahead (w of the predicted next call generated on a side stream)
-    changes nothing: equal slots, a mismatching call size, a reset in between."""
-    import torch
-
-    from paper_2601_08217_b200 import Channel
-
-    w = ttsynth.get("c4").scaled(ues=3, n_per_call=6_000, calls=5)
-    run = Run(w, seed=17)
-    ref = run.gpu(cuda_device)
-    calls = [6_000, 6_000, 5_000, 7_000, 6_000]  # hits, a miss, a miss, a hit-less restart
-    for la in (6_000, 7_000):
-        ch = Channel(run.delays, w.S, seed=17, snapshot_capacity=run.K, device=cuda_device)
-        ch.load_snapshots(torch.from_numpy(run.gains).to(cuda_device), 0)
-        ch.set_noise_lookahead(la)
-        out, pos = [], 0
-        for n in calls:
-            xs = torch.from_numpy(np.ascontiguousarray(run.x[:, pos:pos + n])).to(cuda_device)
-            out.append(ch.apply(xs, noise_sigma=run.sigma).cpu().numpy())
-            pos += n
-        y = np.concatenate(out, axis=1)
-        assert np.array_equal(y, ref), la
-        # reset and replay the first two slots: lookahead must not leak across the reset
-        ch.reset()
-        again = [ch.apply(torch.from_numpy(np.ascontiguousarray(run.x[:, i * 6_000:(i + 1) * 6_000])).to(cuda_device),
-                          noise_sigma=run.sigma).cpu().numpy() for i in range(2)]
-        assert np.array_equal(np.concatenate(again, axis=1), ref[:, :12_000])
-        ch.close()

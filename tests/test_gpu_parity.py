@@ -187,3 +187,46 @@ def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     assert np.array_equal(outs["rw"], outs["tiled"])
     assert np.array_equal(outs["rw"], outs["generic"])
     compare(outs["rw"], run.oracle(), name)
+
+
+@pytest.mark.parametrize("case", ["max_delay", "many_taps", "one_sample_calls", "unaligned_rows"])
+def test_edge_cases(cuda_device, case):
+    """Edge cases of the boundary: the largest delay (TT_MAX_DELAY), very many taps,
+    1-sample calls (every call shorter than the delay line), and input / output rows
+    that start 8 B off a 16-B boundary (the TMA staging splits off an 8-B head)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    if case == "max_delay":
+        w = ttsynth.get("c1").scaled(fixed_delays=(0, 4096), fixed_pdp=(0.5, 0.5), L=2, D=4096, S=64,
+                                     n_per_call=9_001)
+        calls = [5_000, 4_001]
+    elif case == "many_taps":
+        w = ttsynth.get("c2").scaled(ues=1, L=2000, D=4000, S=512, n_per_call=6_000, snr_db=10.0)
+        calls = [6_000]
+    elif case == "one_sample_calls":
+        w = ttsynth.get("c3").scaled(ues=1, dirs=2, n_per_call=40, calls=1)
+        calls = [1] * 40
+    else:
+        w = ttsynth.get("c4").scaled(ues=2, n_per_call=5_001, calls=1)
+        calls = [5_001]
+    run = Run(w, seed=23)
+    if case != "unaligned_rows":
+        y = run.gpu(cuda_device, calls=calls)
+    else:
+        ch = Channel(run.delays, w.S, seed=23, snapshot_capacity=run.K, device=cuda_device)
+        ch.load_snapshots(torch.from_numpy(run.gains).to(cuda_device), 0)
+        n = calls[0]
+        big_x = torch.zeros((run.C * n + 1) * 2, dtype=torch.float32, device=cuda_device)
+        big_y = torch.zeros_like(big_x)
+        xs = big_x[2:].view(run.C, n, 2)  # 8 B past a 16-B boundary
+        xs.copy_(torch.from_numpy(run.x).to(cuda_device))
+        ys = big_y[2:].view(run.C, n, 2)
+        assert xs.data_ptr() % 16 == 8 and ys.data_ptr() % 16 == 8
+        ch.apply(xs, out=ys, noise_sigma=run.sigma)
+        torch.cuda.synchronize()
+        y = ys.cpu().numpy()
+        ch.close()
+        assert np.array_equal(y, run.gpu(cuda_device))
+    compare(y, run.oracle(), case)

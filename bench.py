@@ -180,17 +180,21 @@ def run_reference(args, w):
     import oracle
 
     cores = len(os.sched_getaffinity(0))
-    # each step: one slot of a bounded channel sample, sized for ~2 s per step
+    # each step: one slot of a bounded channel sample, sized for ~1 s of oracle work
     n = w.n_per_call
     K = (n - 1) // w.S + 2
-    c = 1
-    g = ttsynth.snapshots(w, 0, 64, K)
-    x = ttsynth.iq(w, 0, 64, 0)
-    d = ttsynth.delays(w, 0, 64)
+    probe = min(w.C, max(1, cores))
+    d = ttsynth.delays(w, 0, probe)
+    g = ttsynth.snapshots(w, 0, probe, K)
+    x = ttsynth.iq(w, 0, probe, 0)
+    oracle.convolve(d, w.S, g, 0, x, 0, 0, n, sigma=w.sigma)  # library load / thread start
     t0 = time.perf_counter()
-    oracle.convolve(d[:1], w.S, g[:1], 0, x[:1], 0, 0, n, sigma=w.sigma)
-    one = time.perf_counter() - t0
-    c = int(max(1, min(64, 2.0 / max(one, 1e-4))))
+    oracle.convolve(d, w.S, g, 0, x, 0, 0, n, sigma=w.sigma)
+    per_ch = (time.perf_counter() - t0) / probe
+    c = int(max(1, min(w.C, 1.0 / max(per_ch, 1e-6))))
+    d = ttsynth.delays(w, 0, c)
+    g = ttsynth.snapshots(w, 0, c, K)
+    x = ttsynth.iq(w, 0, c, 0)
     for _ in range(args.warmup):
         oracle.convolve(d[:c], w.S, g[:c], 0, x[:c], 0, 0, n, sigma=w.sigma)
     ts = []

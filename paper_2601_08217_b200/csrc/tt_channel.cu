@@ -60,6 +60,7 @@ struct DeviceGuard {
 struct TiledPlan {
     int R = 0;           // outputs per consumer thread (0: does not fit -> generic kernel)
     int CW = 16;         // consumer warps (tile T = CW x 32 x R)
+    int ctas = 1;        // resident CTAs per SM (2 for shapes with <= 8 consumer warps)
     int stages = 2;      // shared-memory pipeline depth (2..4)
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;      // gain rows staged per tile
@@ -143,7 +144,7 @@ cudaError_t prepare_kernel(size_t smem) {
 struct Shape {
     int R, CW;
 };
-constexpr Shape kShapes[] = {{8, 16}, {16, 8}, {4, 16}, {2, 16}};
+constexpr Shape kShapes[] = {{8, 16}, {16, 8}, {8, 8}, {4, 16}, {2, 16}};
 
 template <bool NOISE>
 cudaError_t prepare_tiled(tt_channel_s* h) {
@@ -162,10 +163,13 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     for (const Shape& sh : kShapes) {
         if (fR ? (sh.R != fR || sh.CW != fCW) : (sh.CW != 16)) continue;
         int nk = 0;
-        if (smem_bytes(sh.R, sh.CW, 2, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget) continue;
+        const int ctas = sh.CW <= 8 ? 2 : 1;
+        const size_t budget = ctas == 1 ? kSmemBudget : 112 * 1024;  // 2 CTAs share 228 KB
+        if (smem_bytes(sh.R, sh.CW, 2, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > budget) continue;
         int stages = max_stages;
-        while (stages > 2 && smem_bytes(sh.R, sh.CW, stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > kSmemBudget)
+        while (stages > 2 && smem_bytes(sh.R, sh.CW, stages, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > budget)
             --stages;
+        tp.ctas = ctas;
         tp.R = sh.R;
         tp.CW = sh.CW;
         tp.stages = stages;
@@ -176,6 +180,7 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     switch (tp.R * 100 + tp.CW) {
         case 816: return prepare_kernel<8, 16, NOISE>(tp.smem);
         case 1608: return prepare_kernel<16, 8, NOISE>(tp.smem);
+        case 808: return prepare_kernel<8, 8, NOISE>(tp.smem);
         case 416: return prepare_kernel<4, 16, NOISE>(tp.smem);
         case 216: return prepare_kernel<2, 16, NOISE>(tp.smem);
         default: return cudaSuccess;  // generic kernel
@@ -332,7 +337,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         p.stages = tp.stages;
         if (p.total_super >= (int64_t(1) << 31) || p.total_tiles >= (int64_t(1) << 31))
             return fail(TT_ERR_INVALID_ARG, "call too large: %lld work items", (long long)p.total_super);
-        const int64_t grid = std::min<int64_t>(p.total_super, static_cast<int64_t>(h->num_sms));
+        const int64_t grid = std::min<int64_t>(p.total_super, static_cast<int64_t>(h->num_sms) * tp.ctas);
         const dim3 g(static_cast<unsigned>(grid)), b((tp.CW + 1) * 32);
         const size_t sm = tp.smem;
         // the general variant only when a group sum or sparse offsets are in play
@@ -350,6 +355,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         switch (tp.R * 100 + tp.CW) {
             case 816: TT_LAUNCH(8, 16); break;
             case 1608: TT_LAUNCH(16, 8); break;
+            case 808: TT_LAUNCH(8, 8); break;
             case 416: TT_LAUNCH(4, 16); break;
             default: TT_LAUNCH(2, 16); break;
         }

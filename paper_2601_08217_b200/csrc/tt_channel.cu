@@ -60,7 +60,7 @@ struct DeviceGuard {
 struct TiledPlan {
     int R = 0;           // outputs per consumer thread (0: does not fit -> generic kernel)
     int CW = 16;         // consumer warps (tile T = CW x 32 x R)
-    int ctas = 1;        // resident CTAs per SM (2 for shapes with <= 8 consumer warps)
+    int ctas = 1;        // resident CTAs per SM (2 for shapes with <= 8 consumer warps and R <= 8)
     int stages = 2;      // shared-memory pipeline depth (2..4)
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;      // gain rows staged per tile
@@ -163,7 +163,7 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     for (const Shape& sh : kShapes) {
         if (fR ? (sh.R != fR || sh.CW != fCW) : (sh.CW != 16)) continue;
         int nk = 0;
-        const int ctas = sh.CW <= 8 ? 2 : 1;
+        const int ctas = (sh.CW <= 8 && sh.R <= 8) ? 2 : 1;  // must match the kernel's launch bounds
         const size_t budget = ctas == 1 ? kSmemBudget : 112 * 1024;  // 2 CTAs share 228 KB
         if (smem_bytes(sh.R, sh.CW, 2, h->H, Lr, L4r, h->S, NOISE, sparse, &nk) > budget) continue;
         int stages = max_stages;

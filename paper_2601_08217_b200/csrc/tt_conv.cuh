@@ -484,9 +484,9 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
 
 // CW consumer warps + 1 producer warp; tile T = CW x 32 x R outputs of one channel
 template <int R, int CW, bool NOISE, bool GEN>
-// (shapes with <= 8 consumer warps run two CTAs per SM: independent CTAs drift apart, so
+// (shapes with <= 8 consumer warps and R <= 8 run two CTAs per SM: independent CTAs drift apart, so
 // one CTA's noise epilogue can overlap the other's tap loop; measured slower, opt-in)
-__global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 ? 2 : 1)) tt_conv_kernel(const ConvParams p) {
+__global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt_conv_kernel(const ConvParams p) {
     constexpr int T = CW * 32 * R;
     extern __shared__ __align__(128) unsigned char smem[];
     // layout: [full kMaxStages x 8 B | empty kMaxStages x 8 B | pad to 128][stage 0][stage 1]...

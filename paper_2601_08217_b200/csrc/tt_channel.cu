@@ -841,8 +841,8 @@ tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32
     tt::tt_synth_table_kernel<<<static_cast<unsigned>(std::min<int64_t>((tt + 255) / 256, int64_t(sms) * 16)), 256, 0,
                                 st>>>(num_ue, num_paths, num_sinusoids, nu, static_cast<uint32_t>(seed),
                                       static_cast<uint32_t>(seed >> 32), channel_offset, tab);
-    const int64_t tg = CP * count;
-    tt::tt_synth_gain_kernel<<<static_cast<unsigned>(std::min<int64_t>((tg + 255) / 256, int64_t(sms) * 32)), 256, 0,
+    const int64_t tg = CP * ((count + tt::kSynthBlock - 1) / tt::kSynthBlock);
+    tt::tt_synth_gain_kernel<<<static_cast<unsigned>(std::min<int64_t>((tg + 127) / 128, int64_t(sms) * 32)), 128, 0,
                                st>>>(num_ue, num_paths, num_sinusoids, tab, dtau, dpw, first_index, count,
                                      reinterpret_cast<float2*>(gains_out));
     TT_CUDA(cudaGetLastError(), "synthesis launch");

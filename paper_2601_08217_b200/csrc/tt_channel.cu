@@ -626,9 +626,12 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
     if (h->in_row) return fail(TT_ERR_UNSUPPORTED, "apply_host with an input map: use tt_channel_apply");
     DeviceGuard dg(h->dev);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // chunk of channels per pipeline stage: ~64 MiB of input, at least one channel
+    // chunk of channels per pipeline stage: ~16 MiB of input (short pipeline fill, PCIe
+    // duplex kept busy), at least one channel
     const int64_t per_ch = n_samples;
-    int64_t cc = std::max<int64_t>(1, (int64_t(64) << 20) / (per_ch * 8));
+    const char* fc = getenv("TT_HOST_CHUNK_MB");  // experiments
+    const int64_t chunk_b = (fc ? std::max<int64_t>(1, atoll(fc)) : int64_t(16)) << 20;
+    int64_t cc = std::max<int64_t>(1, chunk_b / (per_ch * 8));
     cc = std::min<int64_t>(cc, h->C);
     const size_t need = static_cast<size_t>(cc * per_ch);
     if (need > h->stage_elems) {

@@ -230,3 +230,48 @@ def test_edge_cases(cuda_device, case):
         ch.close()
         assert np.array_equal(y, run.gpu(cuda_device))
     compare(y, run.oracle(), case)
+
+
+def test_random_instances_vs_oracle(cuda_device):
+    """SPEC AC1-style property sweep: many random instances — channel count,
+    taps, delay span, snapshot period (powers of two and not), noise on/off, random
+    call splits (streamed == one-shot) — each against the oracle. Covers every plan
+    the library picks (tiled R = 8/4/2 with fast / grouped / per-row gain paths, and
+    the generic kernel)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    rng = np.random.default_rng(2026)
+    kinds = set()
+    for inst in range(60):
+        C = int(rng.integers(1, 6))
+        L = int(rng.integers(1, 101))
+        D = int(rng.integers(L - 1, 4 * L + 50)) if L > 1 else int(rng.integers(0, 50))
+        S = int(rng.choice([1, 3, 16, 32, 64, 100, 128, 256, 333, 512, 1024]))
+        N = int(rng.integers(1, 4097))
+        sigma = float(rng.choice([0.0, 0.05]))
+        d = np.stack([np.sort(rng.choice(D + 1, L, replace=D + 1 < L)) for _ in range(C)]).astype(np.int32)
+        K = (N - 1) // S + 2
+        g = (rng.standard_normal((C, K, L, 2)) / np.sqrt(2 * L)).astype(np.float32)
+        x = (rng.standard_normal((C, N, 2)) * np.sqrt(0.5)).astype(np.float32)
+        cuts = np.sort(rng.choice(np.arange(1, N), size=min(int(rng.integers(0, 4)), N - 1), replace=False)) \
+            if N > 1 else np.array([], int)
+        calls = np.diff(np.concatenate([[0], cuts, [N]])).astype(int)
+        outs = []
+        for split in (calls, [N]):
+            ch = Channel(d, S, seed=inst, snapshot_capacity=K, device=cuda_device)
+            kinds.add(int(ch.info().kernel) * 100 + int(ch.info().outputs_per_thread))
+            ch.load_snapshots(torch.from_numpy(g).to(cuda_device), 0)
+            ys, pos = [], 0
+            for n in split:
+                ys.append(ch.apply(torch.from_numpy(np.ascontiguousarray(x[:, pos:pos + n])).to(cuda_device),
+                                   noise_sigma=sigma).cpu().numpy())
+                pos += int(n)
+            ch.close()
+            outs.append(np.concatenate(ys, axis=1))
+        assert np.array_equal(outs[0], outs[1]), (inst, C, L, D, S, N, list(calls))
+        ref = oracle.convolve(d, S, g, 0, x, 0, 0, N, sigma=sigma, seed=inst)
+        if np.abs(ref).max() > 0:
+            compare(outs[0], ref, f"instance {inst}: C={C} L={L} D={D} S={S} N={N}")
+    assert len(kinds) >= 3, kinds  # several plans were exercised

@@ -111,6 +111,7 @@ struct tt_channel_s {
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
     int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
+    bool pdl = true;            // launch the tiled kernel with programmatic dependent launch (TT_PDL=0: off)
     int32_t top_n = 0;          // NEXT f2: taps kept per interval (0 = dense)
     int32_t n4 = 0;             // sparse offsets row stride (>= top_n + 1, multiple of 4)
     float4* sring = nullptr;    // [C][cap][top_n] (+1) compacted rows of the selected taps
@@ -342,15 +343,28 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         const size_t sm = tp.smem;
         // the general variant only when a group sum or sparse offsets are in play
         const bool gen = ar.agg || sparse;
-#define TT_LAUNCH(RR, CC)                                                                 \
-    do {                                                                                  \
-        if (noise) {                                                                      \
-            if (gen) tt::tt_conv_kernel<RR, CC, true, true><<<g, b, sm, st>>>(p);         \
-            else tt::tt_conv_kernel<RR, CC, true, false><<<g, b, sm, st>>>(p);            \
-        } else {                                                                          \
-            if (gen) tt::tt_conv_kernel<RR, CC, false, true><<<g, b, sm, st>>>(p);        \
-            else tt::tt_conv_kernel<RR, CC, false, false><<<g, b, sm, st>>>(p);           \
-        }                                                                                 \
+        // programmatic dependent launch (PDL): back-to-back slot calls overlap the next
+        // grid's launch and CTA set-up with this one's tail (the kernel waits on
+        // griddepcontrol.wait before touching global memory)
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+        cfg.gridDim = g;
+        cfg.blockDim = b;
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+#define TT_LAUNCH(RR, CC)                                                                   \
+    do {                                                                                    \
+        if (noise) {                                                                        \
+            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, true, true>, p);   \
+            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, true, false>, p);      \
+        } else {                                                                            \
+            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, false, true>, p);  \
+            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, false, false>, p);     \
+        }                                                                                   \
     } while (0)
         switch (tp.R * 100 + tp.CW) {
             case 816: TT_LAUNCH(8, 16); break;
@@ -487,6 +501,7 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     h->seed = seed;
     h->cap = snapshot_capacity;
     h->chan_off = channel_offset;
+    if (const char* fp = getenv("TT_PDL")) h->pdl = atoi(fp) != 0;
 
     // per channel: taps sorted by delay (stable: ties keep tap index order); perm[c][j]
     // is the original index of sorted tap j, xoff[c][j] its window offset H - d

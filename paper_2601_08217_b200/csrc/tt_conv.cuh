@@ -513,6 +513,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
         fence_mbar_init();
     }
     __syncthreads();
+    // programmatic dependent launch: the next call's grid may be scheduled now (its CTAs
+    // take over SMs as ours exit); and nothing here touches global memory before the
+    // previous grid on the stream has completed (history, gain ring, y reuse)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == CW) {
         // producer: run ahead of the consumers by up to `stages` tiles

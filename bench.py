@@ -251,9 +251,14 @@ def main():
     rank, world, local = shard.env()
     if world != args.gpus and rank == 0:
         print(f"note: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    pg = shard.init("nccl", dev)
+    # TT_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 with a gloo group, to exercise
+    # the sharded multi-rank path on a one-GPU box (the ranks' kernels are independent)
+    one_gpu = os.environ.get("TT_BENCH_ONE_GPU") == "1"
+    local_dev = 0 if one_gpu else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    pg = shard.init("gloo" if one_gpu else "nccl", dev)
+    red_dev = torch.device("cpu") if one_gpu else dev
 
     # ---- this rank's shard (contiguous UE block; DL/UL of a UE stay together) ----------
     c_lo, c_hi = shard.ue_block(w.ues, w.dirs, rank, world)
@@ -290,7 +295,7 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     shard.barrier(pg)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
             step(xs[(args.warmup + i) % P])
@@ -298,8 +303,8 @@ def main():
         torch.cuda.synchronize()
     shard.barrier(pg)
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]  # ms, one launch each
-    elapsed_max = shard.max_over_ranks(ev[0].elapsed_time(ev[-1]), dev, pg)
-    samples_all = shard.sum_over_ranks(C * n * args.steps, dev, pg)  # units all ranks processed
+    elapsed_max = shard.max_over_ranks(ev[0].elapsed_time(ev[-1]), red_dev, pg)
+    samples_all = shard.sum_over_ranks(C * n * args.steps, red_dev, pg)  # units all ranks processed
     value = samples_all / (elapsed_max / 1e3)
     kernel_s = statistics.mean(per_step) / 1e3
 
@@ -321,8 +326,8 @@ def main():
             ch.apply_host(xh[i % len(xh)], yh, noise_sigma=sigma)
         e1.record(stream)
         torch.cuda.synchronize()
-        te = shard.max_over_ranks(e0.elapsed_time(e1), dev, pg)
-        e2e = {"value": shard.sum_over_ranks(C * n * args.e2e_steps, dev, pg) / (te / 1e3), "unit": "samples/s",
+        te = shard.max_over_ranks(e0.elapsed_time(e1), red_dev, pg)
+        e2e = {"value": shard.sum_over_ranks(C * n * args.e2e_steps, red_dev, pg) / (te / 1e3), "unit": "samples/s",
                "h2d_bytes_per_step": slot_bytes, "d2h_bytes_per_step": slot_bytes,
                "steps": args.e2e_steps, "api": "tt_channel_apply_host (pinned host buffers)"}
     info = ch.info()

@@ -69,7 +69,7 @@ struct Plan {
     int kind = TT_KERNEL_GENERIC;
     TiledPlan tiled[2];  // [noise]
     // register-window kernel (opt-in: TT_KERNEL=rw)
-    int rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
+    int rw_R = 0, rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
     size_t rw_smem = 0;
 };
 
@@ -110,6 +110,7 @@ struct tt_channel_s {
     int32_t* perm = nullptr;   // [C][L] original tap index of sorted tap j
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
+    std::vector<int32_t> sorted_d;  // [C][L] delays in sorted-tap order (host; rebuilds the rw table)
     int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
     bool pdl = true;            // launch the tiled kernel with programmatic dependent launch (TT_PDL=0: off)
     int32_t top_n = 0;          // NEXT f2: taps kept per interval (0 = dense)
@@ -188,6 +189,102 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
     }
 }
 
+// RW-namespace of the register-window kernel with R outputs per thread
+template <int R> struct RwNs;
+template <> struct RwNs<16> {
+    using Params = tt::rw::Params;
+    static constexpr int T = tt::rw::T, kBlockBytes = tt::rw::kBlockBytes, kThreads = tt::rw::kThreads;
+    template <bool NOISE> static constexpr auto kernel() { return tt::rw::tt_conv_rw_kernel<NOISE>; }
+};
+template <> struct RwNs<8> {
+    using Params = tt::rw8::Params;
+    static constexpr int T = tt::rw8::T, kBlockBytes = tt::rw8::kBlockBytes, kThreads = tt::rw8::kThreads;
+    template <bool NOISE> static constexpr auto kernel() { return tt::rw8::tt_conv_rw_kernel<NOISE>; }
+};
+
+// plan + tap table of the register-window kernel: per sorted tap, the byte offset of
+// its window in a thread's doubled block ((o / R) blocks + (o % R) slots, o = Hp - d)
+// and the number of fresh samples min(d_j - d_{j-1}, R) (R for the first tap)
+template <int R>
+cudaError_t prepare_rw(tt_channel_s* h) {
+    using NS = RwNs<R>;
+    const int Hp = h->H - 16;
+    const int nb = (Hp + NS::T) / R;
+    const size_t wbytes = (static_cast<size_t>(nb) * NS::kBlockBytes + 15) & ~size_t(15);
+    const size_t rows = (NS::T - 1) / h->S + 2;
+    const size_t row_stride = static_cast<size_t>(h->L) * 16 + 16;
+    const size_t tbytes = (static_cast<size_t>(h->L + 1) * 8 + 15) & ~size_t(15);
+    const size_t sbytes = wbytes + rows * row_stride + tbytes;
+    const size_t sm = 128 + 2 * sbytes;
+    if (sm > kSmemBudget) return cudaSuccess;  // does not fit: tiled kernel
+    std::vector<int2> tb(static_cast<size_t>(h->C) * (h->L + 1), int2{0, 0});
+    for (int c = 0; c < h->C; ++c) {
+        const int32_t* dc = h->sorted_d.data() + static_cast<size_t>(c) * h->L;
+        for (int j = 0; j < h->L; ++j) {
+            const int o = Hp - dc[j];
+            const int gap = j == 0 ? R : std::min(R, dc[j] - dc[j - 1]);
+            tb[static_cast<size_t>(c) * (h->L + 1) + j] = int2{(o / R) * NS::kBlockBytes + (o % R) * 8, gap};
+        }
+    }
+    cudaError_t e;
+    if ((e = cudaMemcpy(h->tab, tb.data(), tb.size() * sizeof(int2), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(NS::template kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sm))) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(NS::template kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sm))) != cudaSuccess)
+        return e;
+    h->plan.rw_R = R;
+    h->plan.rw_wbytes = static_cast<int>(wbytes);
+    h->plan.rw_rows = static_cast<int>(rows);
+    h->plan.rw_row_stride = static_cast<int>(row_stride);
+    h->plan.rw_sbytes = static_cast<int>(sbytes);
+    h->plan.rw_smem = sm;
+    return cudaSuccess;
+}
+
+// launch the register-window kernel with R outputs per thread
+template <int R>
+void launch_rw(tt_channel_s* h, const tt::ConvParams& p, const float2* x, float2* y, int32_t c_lo, int nch, int64_t n,
+               bool noise, cudaStream_t st) {
+    using NS = RwNs<R>;
+    typename NS::Params q{};
+    q.x = x;
+    q.y = y;
+    q.hist_rd = p.hist_rd;
+    q.hist_wr = p.hist_wr;
+    q.ring = h->ring;
+    q.tab = h->tab;
+    q.n = n;
+    q.t = h->t;
+    q.cap = h->cap;
+    q.chan_offset = h->chan_off;
+    q.c_lo = c_lo;
+    q.L = h->L;
+    q.H = h->H;
+    q.Hp = h->H - 16;
+    q.S = h->S;
+    q.a = static_cast<int32_t>(h->t & (R - 1));
+    q.nb = (q.Hp + NS::T) / R;
+    q.s_shift = p.s_shift;
+    q.inv_S = p.inv_S;
+    q.key0 = p.key0;
+    q.key1 = p.key1;
+    q.noise_sc = p.noise_sc;
+    q.vec_store = ((n & 1) == 0 && (q.a & 1) == 0) ? 1 : 0;
+    q.rows = h->plan.rw_rows;
+    q.row_stride = h->plan.rw_row_stride;
+    q.wbytes = h->plan.rw_wbytes;
+    q.sbytes = h->plan.rw_sbytes;
+    q.tiles_per_ch = static_cast<int32_t>((n + q.a + NS::T - 1) / NS::T);
+    q.total_tiles = static_cast<int64_t>(nch) * q.tiles_per_ch;
+    const int64_t grid = std::min<int64_t>(q.total_tiles, static_cast<int64_t>(h->num_sms));
+    if (noise)
+        NS::template kernel<true>()<<<static_cast<unsigned>(grid), NS::kThreads, h->plan.rw_smem, st>>>(q);
+    else
+        NS::template kernel<false>()<<<static_cast<unsigned>(grid), NS::kThreads, h->plan.rw_smem, st>>>(q);
+}
+
 cudaError_t prepare_plan(tt_channel_s* h) {
     h->plan = Plan{};
     // TT_KERNEL=rw|tiled|generic selects the kernel (all are bit-identical; default tiled)
@@ -195,31 +292,12 @@ cudaError_t prepare_plan(tt_channel_s* h) {
     const bool want_rw = force && !strcmp(force, "rw");
     const bool want_generic = force && !strcmp(force, "generic");
     if (want_generic) return cudaSuccess;
-    // register-window kernel: needs 16-aligned snapshot intervals and two window stages
-    // of (Hp + T) / 16 doubled blocks in shared memory
-    if (want_rw && h->S % 16 == 0) {
-        const int Hp = h->H - 16;
-        const int nb = (Hp + tt::rw::T) / 16;
-        const size_t wbytes = (static_cast<size_t>(nb) * tt::rw::kBlockBytes + 15) & ~size_t(15);
-        const size_t rows = (tt::rw::T - 1) / h->S + 2;
-        const size_t row_stride = static_cast<size_t>(h->L) * 16 + 16;
-        const size_t tbytes = (static_cast<size_t>(h->L + 1) * 8 + 15) & ~size_t(15);
-        const size_t sbytes = wbytes + rows * row_stride + tbytes;
-        const size_t sm = 128 + 2 * sbytes;
-        if (sm <= kSmemBudget) {
-            h->plan.rw_wbytes = static_cast<int>(wbytes);
-            h->plan.rw_rows = static_cast<int>(rows);
-            h->plan.rw_row_stride = static_cast<int>(row_stride);
-            h->plan.rw_sbytes = static_cast<int>(sbytes);
-            h->plan.rw_smem = sm;
-            cudaError_t e;
-            if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sm))) != cudaSuccess)
-                return e;
-            if ((e = cudaFuncSetAttribute(tt::rw::tt_conv_rw_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sm))) != cudaSuccess)
-                return e;
-        }
+    // register-window kernel (R = 16 or 8 consecutive outputs per thread): needs
+    // R-aligned snapshot intervals and two window stages of (Hp + T) / R doubled blocks
+    const bool want_rw8 = force && !strcmp(force, "rw8");
+    if ((want_rw || want_rw8) && h->S % 16 == 0) {
+        cudaError_t e = want_rw8 ? prepare_rw<tt::rw8::R>(h) : prepare_rw<tt::rw::R>(h);
+        if (e != cudaSuccess) return e;
     }
     // tiled plans (also behind the rw kernel: aggregation and input maps use them)
     cudaError_t e;
@@ -282,41 +360,8 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
     if (h->plan.kind == TT_KERNEL_RW && !ar.agg && !h->in_row && !sparse) {
-        tt::rw::Params q{};
-        q.x = x;
-        q.y = y;
-        q.hist_rd = p.hist_rd;
-        q.hist_wr = p.hist_wr;
-        q.ring = h->ring;
-        q.tab = h->tab;
-        q.n = n;
-        q.t = h->t;
-        q.cap = h->cap;
-        q.chan_offset = h->chan_off;
-        q.c_lo = c_lo;
-        q.L = h->L;
-        q.H = h->H;
-        q.Hp = h->H - 16;
-        q.S = h->S;
-        q.a = static_cast<int32_t>(h->t & 15);
-        q.nb = (q.Hp + tt::rw::T) / 16;
-        q.s_shift = p.s_shift;
-        q.inv_S = p.inv_S;
-        q.key0 = p.key0;
-        q.key1 = p.key1;
-        q.noise_sc = p.noise_sc;
-        q.vec_store = ((n & 1) == 0 && (q.a & 1) == 0) ? 1 : 0;
-        q.rows = h->plan.rw_rows;
-        q.row_stride = h->plan.rw_row_stride;
-        q.wbytes = h->plan.rw_wbytes;
-        q.sbytes = h->plan.rw_sbytes;
-        q.tiles_per_ch = static_cast<int32_t>((n + q.a + tt::rw::T - 1) / tt::rw::T);
-        q.total_tiles = static_cast<int64_t>(nch) * q.tiles_per_ch;
-        const int64_t grid = std::min<int64_t>(q.total_tiles, static_cast<int64_t>(h->num_sms));
-        if (noise)
-            tt::rw::tt_conv_rw_kernel<true><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
-        else
-            tt::rw::tt_conv_rw_kernel<false><<<static_cast<unsigned>(grid), tt::rw::kThreads, h->plan.rw_smem, st>>>(q);
+        if (h->plan.rw_R == 8) launch_rw<8>(h, p, x, y, c_lo, nch, n, noise, st);
+        else launch_rw<16>(h, p, x, y, c_lo, nch, n, noise, st);
     } else if (h->plan.tiled[noise ? 1 : 0].R != 0 &&
                (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row || sparse)) {
         const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
@@ -506,22 +551,16 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     // per channel: taps sorted by delay (stable: ties keep tap index order); perm[c][j]
     // is the original index of sorted tap j, xoff[c][j] its window offset H - d
     std::vector<int32_t> pm(static_cast<size_t>(CL)), xo(static_cast<size_t>(num_ue) * h->L4, 0);
-    // register-window table: per sorted tap, the byte offset of its window in a thread's
-    // doubled block ((o >> 4) blocks + (o & 15) slots, o = Hp - d) and the number of fresh
-    // samples min(d_j - d_{j-1}, 16) (16 for the first tap); entry L is padding
-    std::vector<int2> tb(static_cast<size_t>(num_ue) * (num_taps + 1), int2{0, 0});
+    // (the register-window table is built by its plan, prepare_rw)
+    const size_t tb_elems = static_cast<size_t>(num_ue) * (num_taps + 1);
+    h->sorted_d.assign(static_cast<size_t>(CL), 0);
     for (int c = 0; c < num_ue; ++c) {
         int32_t* pc = pm.data() + static_cast<size_t>(c) * num_taps;
         std::iota(pc, pc + num_taps, 0);
         const int32_t* dc = delays + static_cast<int64_t>(c) * num_taps;
         std::stable_sort(pc, pc + num_taps, [dc](int32_t a, int32_t b) { return dc[a] < dc[b]; });
         for (int j = 0; j < num_taps; ++j) xo[static_cast<size_t>(c) * h->L4 + j] = h->H - dc[pc[j]];
-        const int Hp = h->H - 16;
-        for (int j = 0; j < num_taps; ++j) {
-            const int o = Hp - dc[pc[j]];
-            const int gap = j == 0 ? 16 : std::min(16, dc[pc[j]] - dc[pc[j - 1]]);
-            tb[static_cast<size_t>(c) * (num_taps + 1) + j] = int2{(o >> 4) * tt::rw::kBlockBytes + (o & 15) * 8, gap};
-        }
+        for (int j = 0; j < num_taps; ++j) h->sorted_d[static_cast<size_t>(c) * num_taps + j] = dc[pc[j]];
     }
     auto bail = [&](tt_status s) {
         free_all(h);
@@ -531,7 +570,7 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     cudaError_t e;
     // + one float4: the kernels prefetch one tap ahead
     const size_t ring_b = (static_cast<size_t>(num_ue) * snapshot_capacity * num_taps + 1) * sizeof(float4);
-    const size_t tb_b = tb.size() * sizeof(int2);
+    const size_t tb_b = tb_elems * sizeof(int2);
     const size_t hist_b = 2 * static_cast<size_t>(num_ue) * h->H * sizeof(float2);
     const size_t pm_b = pm.size() * sizeof(int32_t), xo_b = xo.size() * sizeof(int32_t);
     if ((e = cudaMalloc(&h->ring, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(snapshot ring)"));
@@ -540,7 +579,7 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     if ((e = cudaMalloc(&h->xoff, xo_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(xoff)"));
     if ((e = cudaMalloc(&h->tab, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(tab)"));
     h->dev_bytes = ring_b + hist_b + pm_b + xo_b + tb_b;
-    if ((e = cudaMemcpy(h->tab, tb.data(), tb_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy tab"));
+    if ((e = cudaMemset(h->tab, 0, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "zero tab"));
     if ((e = cudaMemcpy(h->perm, pm.data(), pm_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
     if ((e = cudaMemcpy(h->xoff, xo.data(), xo_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy xoff"));
     if (hist_b && (e = cudaMemset(h->hist, 0, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "zero history"));
@@ -899,7 +938,7 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
                                               h->agg_scratch_elems * sizeof(float2));
     info->kernel = h->plan.kind;
     info->top_n = h->top_n;
-    info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? tt::rw::R
+    info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? h->plan.rw_R
                                : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R : 0;
     info->launches_per_apply = h->plan.kind == TT_KERNEL_GENERIC ? 2 : 1;
     return TT_OK;

@@ -180,11 +180,12 @@ def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     w = ttsynth.get(name).scaled(**kw)
     run = Run(w, seed=21)
     outs = {}
-    for k in ("rw", "tiled", "generic"):
+    for k in ("rw", "rw8", "tiled", "generic"):
         monkeypatch.setenv("TT_KERNEL", k)
         outs[k] = run.gpu(cuda_device, calls=calls)
     monkeypatch.delenv("TT_KERNEL")
     assert np.array_equal(outs["rw"], outs["tiled"])
+    assert np.array_equal(outs["rw8"], outs["tiled"])
     assert np.array_equal(outs["rw"], outs["generic"])
     compare(outs["rw"], run.oracle(), name)
 

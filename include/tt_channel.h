@@ -153,7 +153,7 @@ tt_status tt_channel_set_top_n(tt_channel_t h, int32_t top_n);
  * Errors: INVALID_ARG (NULL handle, num_rows <= 0, a row outside [0, num_rows)), CUDA. */
 tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t num_rows);
 
-#define TT_AGG_CHUNK 16 /* channels per partial sum of tt_channel_apply_aggregate */
+#define TT_AGG_CHUNK 8 /* channels per partial sum of tt_channel_apply_aggregate */
 
 /* NEXT f1 ("the gNB ... applies convolution independently for each UE ...
  * and only then aggregates them"; P:330 UE-localised convolution) and f4: apply the

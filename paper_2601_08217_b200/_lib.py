@@ -23,7 +23,7 @@ STATUS = {
 }
 TT_MAX_DELAY = 4096
 TT_MAX_TAPS = 4096
-TT_AGG_CHUNK = 16
+TT_AGG_CHUNK = 8
 
 # functions declared in include/tt_channel.h (tests/test_abi.py checks the header agrees)
 EXPORTS = (

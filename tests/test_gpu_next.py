@@ -14,7 +14,7 @@ from harness import Run, compare, to_c
 
 pytestmark = pytest.mark.gpu
 
-CHUNK = 16  # TT_AGG_CHUNK
+CHUNK = 8  # TT_AGG_CHUNK
 
 
 def _chunked_sum_f32(y, G):

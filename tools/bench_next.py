@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Measurement of the NEXT rows on one GPU, one JSON line each.
 
-    python tools/bench_next.py [--steps K] [--warmup W] [--modes aggregate,sparse,links,synth]
+    python tools/bench_next.py [--steps K] [--warmup W] [--modes aggregate,sparse,links,synth,load]
 
 Workloads (synthetic, built from BASELINE c4: 122.88 Msps, 0.5 ms slots of 61,440
 samples, 48 taps in [0, 1024], S = 256):
@@ -13,6 +13,7 @@ samples, 48 taps in [0, 1024], S = 256):
                   UE (tt_channel_set_input_map + aggregate, G = 3)
   synth     (f3)  Jakes synthesis of one slot's snapshots for c4's 1024 channels
                   (24 paths -> 48 grid taps, M = 32 sinusoids, 240 snapshots per slot)
+  load      (a1)  one c4 slot of snapshots loaded from a device buffer into the ring
 Device-timed with CUDA events over K steps after W warm-up steps; inputs resident.
 """
 from __future__ import annotations
@@ -184,11 +185,39 @@ def run_synth(args, dev, peaks, P=24, M=32):
           "note": "includes host path validation, table build and a stream sync per call"})
 
 
+def run_load(args, dev, peaks):
+    """a1: snapshot loading as a streaming user does it — one slot's snapshots (c4: 1024
+    channels x 240 snapshots x 48 taps) copied from a device buffer into the ring each
+    step (tt_channel_load_snapshots -> tt_load_kernel: tap sort + (g, dg) rows)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    w = ttsynth.get("c4")
+    C = w.C
+    per = w.n_per_call // w.S
+    steps_total = args.warmup + args.steps + 2
+    g = ttsynth.snapshots(w, 0, C, steps_total * per + 1, backend="torch", device=dev)
+    ch = Channel(ttsynth.delays(w), w.S, seed=1, snapshot_capacity=4 * per, device=dev)
+    blocks = [g[:, i * per:(i + 1) * per].contiguous() for i in range(steps_total)]
+    el, pr, clk = timed(lambda i: ch.load_snapshots(blocks[i], i * per), args.steps, args.warmup,
+                        torch.cuda.current_stream())
+    ch.close()
+    ms = el / args.steps
+    nbytes = C * per * w.L * (8 + 16)  # read (g) + write (g, dg) per tap-snapshot
+    line("load", "tap-snapshots loaded per s", C * per * w.L / (ms / 1e3), "tap-snapshots/s", args.steps,
+         args.warmup, ms, pr, clk,
+         {"workload": "c4: one slot of snapshots (1024 x 240 x 48) per step, device source (row a1)",
+          "channels": C, "snapshots_per_step": per, "taps": w.L},
+         {"roofline": {"bound": "hbm", "achieved": nbytes / (ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                       "frac": nbytes / (ms / 1e3) / 1e9 / peaks["hbm_gbs"]}})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--modes", default="aggregate,sparse,links,synth")
+    ap.add_argument("--modes", default="aggregate,sparse,links,synth,load")
     args = ap.parse_args()
     import torch
 
@@ -196,7 +225,8 @@ def main():
     torch.cuda.set_device(dev)
     peaks = bench._peaks()
     for m in args.modes.split(","):
-        {"aggregate": run_aggregate, "sparse": run_sparse, "links": run_links, "synth": run_synth}[m](args, dev, peaks)
+        {"aggregate": run_aggregate, "sparse": run_sparse, "links": run_links, "synth": run_synth,
+         "load": run_load}[m](args, dev, peaks)
         torch.cuda.empty_cache()
 
 

@@ -93,3 +93,16 @@ def test_null_handle_calls_fail_cleanly(tt):
     assert L.tt_channel_reset(None, None) == 1
     assert L.tt_channel_get_info(None, None) == 1
     assert L.tt_channel_destroy(None) == 0
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the CUDA library every call raises (here via TT_LIB
+    pointing at a path that does not exist, in a fresh interpreter)."""
+    import subprocess
+    import sys
+
+    code = ("import paper_2601_08217_b200._lib as L\n"
+            "try:\n    L.lib()\nexcept ImportError as e:\n    print('raised', e)\n")
+    env = dict(os.environ, TT_LIB=str(tmp_path / "nope.so"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert "raised" in r.stdout and "no fallback" in r.stdout, r.stdout + r.stderr

@@ -127,6 +127,16 @@ def roofline(w: ttsynth.Workload, samples: int, kernel_s: float, peaks: dict, tr
     return rl
 
 
+def _ceilings(w, peaks, achieved_sps):
+    f = peaks["sm_max_mhz"] * 1e6
+    interp = SM_COUNT_NOMINAL * FP32_LANES_PER_SM * f / (6.0 * w.L)   # samples/s
+    smem = SM_COUNT_NOMINAL * 16.0 * f / w.L                           # 16 output-taps/clk/SM
+    hbm = peaks["hbm_gbs"] * 1e9 / (16.0 + 16.0 * w.L / w.S)          # incl. the gain stream
+    lim = min(interp, smem, hbm)
+    return {"interp_fp32_sps": interp, "smem_operands_sps": smem, "hbm_with_gains_sps": hbm,
+            "frac_of_min": achieved_sps / lim}
+
+
 def _traffic(config: str):
     """dram read+write bytes per launch from the committed ncu --set full summary."""
     try:
@@ -345,6 +355,10 @@ def main():
             "roofline": rl,
             "realtime_ues": w.realtime_ues(value),
             "ns_fraction_box": value / (world * rl["ns_samples_per_s_per_gpu"]),
+            # design ceilings below NS, per GPU: exact per-sample
+            # interpolation (6 FMA lanes per output-tap instead of 4) and one 8-B shared-
+            # memory operand read per output-tap (128 B/clk/SM)
+            "ceilings": _ceilings(w, peaks, C * n / kernel_s),
             "call_ms": {"p50": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
                         "slot_ms": 1e3 * n / w.rate_sps},
             "gpu_launches": args.steps * int(info.launches_per_apply),

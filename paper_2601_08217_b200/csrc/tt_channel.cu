@@ -125,10 +125,12 @@ struct tt_channel_s {
     size_t dev_bytes = 0;
     Plan plan;
     // host-buffer path
-    float2* stage = nullptr;  // 3 x (in + out) chunk buffers
+    static constexpr int kHostBufs = 4;  // (in + out) chunk buffers in flight
+    float2* stage = nullptr;  // kHostBufs x (in + out) chunk buffers
     size_t stage_elems = 0;   // float2 per in (or out) chunk buffer
-    cudaStream_t cs_h2d = nullptr, cs_d2h = nullptr;
-    cudaEvent_t ev_h2d[3] = {}, ev_k[3] = {}, ev_free[3] = {}, ev_start = nullptr;
+    cudaStream_t cs_h2d[2] = {}, cs_d2h[2] = {};  // two copy streams per direction
+    cudaEvent_t ev_h2d[kHostBufs] = {}, ev_k[kHostBufs] = {}, ev_free[kHostBufs] = {}, ev_start = nullptr;
+    cudaEvent_t ev_done[2] = {};
 };
 
 namespace {
@@ -479,14 +481,17 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->agg_scratch);
     cudaFree(h->load_stage);
     cudaFree(h->stage);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < tt_channel_s::kHostBufs; ++i) {
         if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
         if (h->ev_k[i]) cudaEventDestroy(h->ev_k[i]);
         if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
     }
     if (h->ev_start) cudaEventDestroy(h->ev_start);
-    if (h->cs_h2d) cudaStreamDestroy(h->cs_h2d);
-    if (h->cs_d2h) cudaStreamDestroy(h->cs_d2h);
+    for (int i = 0; i < 2; ++i) {
+        if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+        if (h->cs_h2d[i]) cudaStreamDestroy(h->cs_h2d[i]);
+        if (h->cs_d2h[i]) cudaStreamDestroy(h->cs_d2h[i]);
+    }
 }
 
 }  // namespace
@@ -688,53 +693,62 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
     int64_t cc = std::max<int64_t>(1, chunk_b / (per_ch * 8));
     cc = std::min<int64_t>(cc, h->C);
     const size_t need = static_cast<size_t>(cc * per_ch);
+    constexpr int NB = tt_channel_s::kHostBufs;
     if (need > h->stage_elems) {
         if (h->stage) {
-            TT_CUDA(cudaStreamSynchronize(h->cs_d2h), "staging drain");
+            TT_CUDA(cudaStreamSynchronize(h->cs_d2h[0]), "staging drain");
+            TT_CUDA(cudaStreamSynchronize(h->cs_d2h[1]), "staging drain");
             cudaFree(h->stage);
             h->stage = nullptr;
             h->stage_elems = 0;
         }
-        TT_CUDA(cudaMalloc(&h->stage, need * 6 * sizeof(float2)), "cudaMalloc(host-path staging)");
+        TT_CUDA(cudaMalloc(&h->stage, need * 2 * NB * sizeof(float2)), "cudaMalloc(host-path staging)");
         h->stage_elems = need;
-        if (!h->cs_h2d) {
-            TT_CUDA(cudaStreamCreateWithFlags(&h->cs_h2d, cudaStreamNonBlocking), "stream create");
-            TT_CUDA(cudaStreamCreateWithFlags(&h->cs_d2h, cudaStreamNonBlocking), "stream create");
-            for (int i = 0; i < 3; ++i) {
+        if (!h->cs_h2d[0]) {
+            for (int k = 0; k < 2; ++k) {
+                TT_CUDA(cudaStreamCreateWithFlags(&h->cs_h2d[k], cudaStreamNonBlocking), "stream create");
+                TT_CUDA(cudaStreamCreateWithFlags(&h->cs_d2h[k], cudaStreamNonBlocking), "stream create");
+                TT_CUDA(cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming), "event create");
+            }
+            for (int i = 0; i < NB; ++i) {
                 TT_CUDA(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming), "event create");
                 TT_CUDA(cudaEventCreateWithFlags(&h->ev_k[i], cudaEventDisableTiming), "event create");
                 TT_CUDA(cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming), "event create");
-                TT_CUDA(cudaEventRecord(h->ev_free[i], h->cs_d2h), "event record");
+                TT_CUDA(cudaEventRecord(h->ev_free[i], h->cs_d2h[i & 1]), "event record");
             }
             TT_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event create");
         }
     }
-    // the copy streams start after everything already enqueued on `stream`
+    // the copy streams start after everything already enqueued on `stream`; chunk i uses
+    // buffer i % NB and the copy streams of parity i % 2 (two DMA queues per direction
+    // keep the PCIe link busier in both directions)
     TT_CUDA(cudaEventRecord(h->ev_start, st), "event record");
-    TT_CUDA(cudaStreamWaitEvent(h->cs_h2d, h->ev_start, 0), "stream wait");
+    for (int k = 0; k < 2; ++k) TT_CUDA(cudaStreamWaitEvent(h->cs_h2d[k], h->ev_start, 0), "stream wait");
     const float2* hin = reinterpret_cast<const float2*>(in);
     float2* hout = reinterpret_cast<float2*>(out);
     int i = 0;
     for (int64_t c0 = 0; c0 < h->C; c0 += cc, ++i) {
-        const int b = i % 3;
+        const int b = i % NB, q = i & 1;
         const int64_t c1 = std::min<int64_t>(h->C, c0 + cc);
         const size_t bytes = static_cast<size_t>((c1 - c0) * per_ch) * sizeof(float2);
         float2* din = h->stage + static_cast<size_t>(b) * 2 * need;
         float2* dout = din + need;
-        TT_CUDA(cudaStreamWaitEvent(h->cs_h2d, h->ev_free[b], 0), "stream wait");
-        TT_CUDA(cudaMemcpyAsync(din, hin + c0 * per_ch, bytes, cudaMemcpyHostToDevice, h->cs_h2d), "H2D");
-        TT_CUDA(cudaEventRecord(h->ev_h2d[b], h->cs_h2d), "event record");
+        TT_CUDA(cudaStreamWaitEvent(h->cs_h2d[q], h->ev_free[b], 0), "stream wait");
+        TT_CUDA(cudaMemcpyAsync(din, hin + c0 * per_ch, bytes, cudaMemcpyHostToDevice, h->cs_h2d[q]), "H2D");
+        TT_CUDA(cudaEventRecord(h->ev_h2d[b], h->cs_h2d[q]), "event record");
         TT_CUDA(cudaStreamWaitEvent(st, h->ev_h2d[b], 0), "stream wait");
         s = launch(h, din, dout, static_cast<int32_t>(c0), static_cast<int32_t>(c1), n_samples, noise_sigma, st);
         if (s != TT_OK) return s;
         TT_CUDA(cudaEventRecord(h->ev_k[b], st), "event record");
-        TT_CUDA(cudaStreamWaitEvent(h->cs_d2h, h->ev_k[b], 0), "stream wait");
-        TT_CUDA(cudaMemcpyAsync(hout + c0 * per_ch, dout, bytes, cudaMemcpyDeviceToHost, h->cs_d2h), "D2H");
-        TT_CUDA(cudaEventRecord(h->ev_free[b], h->cs_d2h), "event record");
+        TT_CUDA(cudaStreamWaitEvent(h->cs_d2h[q], h->ev_k[b], 0), "stream wait");
+        TT_CUDA(cudaMemcpyAsync(hout + c0 * per_ch, dout, bytes, cudaMemcpyDeviceToHost, h->cs_d2h[q]), "D2H");
+        TT_CUDA(cudaEventRecord(h->ev_free[b], h->cs_d2h[q]), "event record");
     }
     // `stream` reaches this point only when every D2H has landed
-    TT_CUDA(cudaEventRecord(h->ev_start, h->cs_d2h), "event record");
-    TT_CUDA(cudaStreamWaitEvent(st, h->ev_start, 0), "stream wait");
+    for (int k = 0; k < 2; ++k) {
+        TT_CUDA(cudaEventRecord(h->ev_done[k], h->cs_d2h[k]), "event record");
+        TT_CUDA(cudaStreamWaitEvent(st, h->ev_done[k], 0), "stream wait");
+    }
     h->t += n_samples;
     if (h->H > 0) h->p ^= 1;
     return TT_OK;
@@ -933,7 +947,7 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->resident_hi = h->res_hi;
     info->channel_offset = h->chan_off;
     info->seed = h->seed;
-    info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 6 * sizeof(float2) +
+    info->device_bytes = static_cast<int64_t>(h->dev_bytes + h->stage_elems * 2 * tt_channel_s::kHostBufs * sizeof(float2) +
                                               h->load_stage_elems * sizeof(float2) +
                                               h->agg_scratch_elems * sizeof(float2));
     info->kernel = h->plan.kind;

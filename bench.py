@@ -61,7 +61,7 @@ class ClockSampler:
 
     def __init__(self, index: int, period_s: float = 0.01):
         self.index, self.period = index, period_s
-        self.samples, self.reasons = [], 0
+        self.samples, self.reasons, self.power = [], 0, []
         self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
@@ -80,6 +80,7 @@ class ClockSampler:
             try:
                 self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
                 self.reasons |= int(self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+                self.power.append(self._nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)  # W
             except Exception:
                 pass
             time.sleep(self.period)
@@ -100,7 +101,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         names = [k for k, v in {**self.BAD, **self.NOTE}.items() if self.reasons & v]
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
-                "reasons": names, "samples": len(self.samples)}
+                "reasons": names, "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power) if self.power else None}
 
 
 def _dist():

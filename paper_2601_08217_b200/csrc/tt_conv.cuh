@@ -160,6 +160,8 @@ struct TileInfo {
 
 // 32-bit index math only: w < 2^31 tiles, i0 < 2^31 samples per call; the global
 // start t enters through the host-precomputed t / S and t % S.
+__host__ __device__ constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2_c(v / 2); }
+
 __device__ __forceinline__ uint32_t div_S(const ConvParams& p, uint32_t v) {
     return p.s_shift >= 0 ? (v >> p.s_shift) : v / static_cast<uint32_t>(p.S);
 }
@@ -189,6 +191,26 @@ __device__ __forceinline__ SuperInfo super_info(const ConvParams& p, int64_t su6
     si.kcount = left < p.chunk ? left : p.chunk;
     return si;
 }
+
+// (channel, tile) of the work items blockIdx.x, blockIdx.x + gridDim.x, ... of the plain
+// variant, advanced without a division per item
+struct TileWalk {
+    uint32_t cl, tl, dcl, dtl, tpc;
+    __device__ __forceinline__ explicit TileWalk(uint32_t tiles_per_ch)
+        : cl(blockIdx.x / tiles_per_ch),
+          tl(blockIdx.x % tiles_per_ch),
+          dcl(gridDim.x / tiles_per_ch),
+          dtl(gridDim.x % tiles_per_ch),
+          tpc(tiles_per_ch) {}
+    __device__ __forceinline__ void next() {
+        tl += dtl;
+        cl += dcl;
+        if (tl >= tpc) {
+            tl -= tpc;
+            ++cl;
+        }
+    }
+};
 
 template <int R, int CW>
 __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int32_t c, int32_t tl) {
@@ -344,15 +366,26 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
         // two: then j * (1/S) is exact and equals the correctly rounded quotient)
         float alpha[R];
         int32_t kk[R];
+        // outputs past a tail tile's end are computed but never stored; their coefficient
+        // row is clamped into the staged block
+        if (p.s_shift >= 0) {
+            const uint32_t sh = static_cast<uint32_t>(p.s_shift), mask = static_cast<uint32_t>(p.S) - 1u;
+            const float inv_S = p.inv_S;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const uint32_t jj = static_cast<uint32_t>(ti.j0 + obase + r * 32);
-            const uint32_t k = div_S(p, jj);
-            // outputs past a tail tile's end are computed but never stored; keep their
-            // coefficient row inside the staged block
-            kk[r] = min(static_cast<int32_t>(k), ti.nk - 1);
-            const float jf = __uint2float_rn(jj - k * static_cast<uint32_t>(p.S));
-            alpha[r] = p.s_shift >= 0 ? __fmul_rn(jf, p.inv_S) : __fdiv_rn(jf, __int2float_rn(p.S));
+            for (int r = 0; r < R; ++r) {
+                const uint32_t jj = static_cast<uint32_t>(ti.j0 + obase + r * 32);
+                kk[r] = min(static_cast<int32_t>(jj >> sh), ti.nk - 1);
+                alpha[r] = __fmul_rn(__uint2float_rn(jj & mask), inv_S);
+            }
+        } else {
+            const float Sf = __int2float_rn(p.S);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t jj = static_cast<uint32_t>(ti.j0 + obase + r * 32);
+                const uint32_t k = jj / static_cast<uint32_t>(p.S);
+                kk[r] = min(static_cast<int32_t>(k), ti.nk - 1);
+                alpha[r] = __fdiv_rn(__uint2float_rn(jj - k * static_cast<uint32_t>(p.S)), Sf);
+            }
         }
         float2 A[R], B[R];
 #pragma unroll
@@ -383,8 +416,8 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
                 mac_tap<R>(q3, xb + o.w, alpha, A, B);
             }
             for (; j < p.L; ++j) mac_tap<R>(cf[j], xb + xo[j], alpha, A, B);
-        } else if ((R & (R - 1)) == 0 && p.s_shift >= 5 && (32 * R) % p.S == 0 && (wj0 & (p.S - 1)) == 0 &&
-                   ((32 * R) >> p.s_shift) <= 4 &&
+        } else if ((R & (R - 1)) == 0 && p.s_shift >= 5 && p.s_shift <= ilog2_c(32 * R) &&
+                   (wj0 & (p.S - 1)) == 0 && ((32 * R) >> p.s_shift) <= 4 &&
                    static_cast<int32_t>(kw0) + ((32 * R) >> p.s_shift) <= ti.nk) {  // (tail tiles: rows staged)
             // the warp starts on an interval boundary and spans NG = 32R / S (2 or 4) whole intervals
             const float4* cf = st.coef + static_cast<int64_t>(kw0) * p.L;
@@ -521,38 +554,46 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
 
     if (warp == CW) {
         // producer: run ahead of the consumers by up to `stages` tiles
-        int it = 0;
+        // stage s and its use count kk, advanced incrementally (no runtime division)
+        int s = 0, kk = 0;
+        auto next = [&] {
+            if (++s == p.stages) {
+                s = 0;
+                ++kk;
+            }
+        };
         if constexpr (!GEN) {
             // one channel tile per work item: w -> (channel, tile)
-            for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
-                const int s = it % p.stages;
-                const int kk = it / p.stages;
+            TileWalk tw(static_cast<uint32_t>(p.tiles_per_ch));
+            for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, next(), tw.next()) {
                 if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
-                const uint32_t cl = static_cast<uint32_t>(w) / static_cast<uint32_t>(p.tiles_per_ch);
-                const int32_t tl = static_cast<int32_t>(static_cast<uint32_t>(w) - cl * p.tiles_per_ch);
-                produce_tile<R>(p, tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(cl), tl), stage(s), &full[s], lane);
+                produce_tile<R>(p, tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl)),
+                                stage(s), &full[s], lane);
             }
         } else {
             for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
                 const SuperInfo si = super_info(p, su);
-                for (int32_t k = 0; k < si.kcount; ++k, ++it) {
-                    const int s = it % p.stages;
-                    const int kk = it / p.stages;
+                for (int32_t k = 0; k < si.kcount; ++k, next()) {
                     if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
                     produce_tile<R>(p, tile_info<R, CW>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
                 }
             }
         }
     } else {
-        int it = 0;
+        int s = 0;
+        uint32_t ph = 0;  // parity of the stage's current use
+        auto next = [&] {
+            if (++s == p.stages) {
+                s = 0;
+                ph ^= 1u;
+            }
+        };
         if constexpr (!GEN) {
-            for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, ++it) {
-                const int s = it % p.stages;
-                const int kk = it / p.stages;
-                mbar_wait(&full[s], kk & 1);
-                const uint32_t cl = static_cast<uint32_t>(w) / static_cast<uint32_t>(p.tiles_per_ch);
-                const int32_t tl = static_cast<int32_t>(static_cast<uint32_t>(w) - cl * p.tiles_per_ch);
-                const TileInfo ti = tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(cl), tl);
+            TileWalk tw(static_cast<uint32_t>(p.tiles_per_ch));
+            for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, next(), tw.next()) {
+                mbar_wait(&full[s], ph);
+                const TileInfo ti =
+                    tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl));
                 consume_tile<R, CW, NOISE, false>(p, ti, stage(s), warp, lane, true, nullptr);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
@@ -560,10 +601,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
         } else {
             for (int64_t su = blockIdx.x; su < p.total_super; su += gridDim.x) {
                 const SuperInfo si = super_info(p, su);
-                for (int32_t k = 0; k < si.kcount; ++k, ++it) {
-                    const int s = it % p.stages;
-                    const int kk = it / p.stages;
-                    mbar_wait(&full[s], kk & 1);
+                for (int32_t k = 0; k < si.kcount; ++k, next()) {
+                    mbar_wait(&full[s], ph);
                     const TileInfo ti = tile_info<R, CW>(p, si.c_first + k, si.tl);
                     // the chunk's sum goes straight into the group row, or into its partial row
                     float2* aggdst =

@@ -153,7 +153,7 @@ struct TileInfo {
     int32_t c;      // channel (absolute)
     int64_t i0;     // first output (call-local)
     int32_t Tt;     // outputs in this tile
-    int64_t kb;     // first snapshot interval
+    uint32_t kq;    // first snapshot interval, relative to the call's (t / S)
     int32_t nk;     // intervals touched
     int32_t j0;     // (t + i0) - kb*S
 };
@@ -222,7 +222,7 @@ __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int32_t c, in
     ti.Tt = rem < T ? static_cast<int32_t>(rem) : T;
     const uint32_t u0 = static_cast<uint32_t>(p.t_mod) + static_cast<uint32_t>(ti.i0);  // (t + i0) - (t / S) S
     const uint32_t q0 = div_S(p, u0);
-    ti.kb = p.t_div + q0;
+    ti.kq = q0;
     ti.j0 = static_cast<int32_t>(u0 - q0 * static_cast<uint32_t>(p.S));
     ti.nk = static_cast<int32_t>(div_S(p, static_cast<uint32_t>(ti.j0 + ti.Tt - 1))) + 1;
     return ti;
@@ -253,7 +253,7 @@ __device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo
     const int64_t row = p.in_row ? static_cast<int64_t>(__ldg(p.in_row + ti.c)) : static_cast<int64_t>(ti.c - p.c_lo);
     const Piece bx = make_piece(st.win + (bl - lo), p.x + row * p.n + bl, static_cast<uint32_t>(hi - bl) * 8u);
     // C, D: coefficient rows kb .. kb + nk - 1, wrapping at the ring's capacity
-    const int64_t s0 = ti.kb % p.cap;
+    const int64_t s0 = (p.t_div + ti.kq) % p.cap;
     const int32_t r1 = static_cast<int32_t>((p.cap - s0) < ti.nk ? (p.cap - s0) : ti.nk);
     const float4* ringc = p.ring + static_cast<int64_t>(ti.c) * p.cap * p.L;
     const uint32_t rowb = static_cast<uint32_t>(p.L) * 16u;
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
                 ++kk;
             }
         };
-        if constexpr (!GEN) {
+        if (!GEN || p.agg == nullptr) {
             // one channel tile per work item: w -> (channel, tile)
             TileWalk tw(static_cast<uint32_t>(p.tiles_per_ch));
             for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, next(), tw.next()) {
@@ -588,13 +588,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
                 ph ^= 1u;
             }
         };
-        if constexpr (!GEN) {
+        if (!GEN || p.agg == nullptr) {
             TileWalk tw(static_cast<uint32_t>(p.tiles_per_ch));
             for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, next(), tw.next()) {
                 mbar_wait(&full[s], ph);
                 const TileInfo ti =
                     tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl));
-                consume_tile<R, CW, NOISE, false>(p, ti, stage(s), warp, lane, true, nullptr);
+                consume_tile<R, CW, NOISE, GEN>(p, ti, stage(s), warp, lane, true, nullptr);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }

@@ -223,7 +223,7 @@ def run_realtime(args, dev, peaks):
 
     base = ttsynth.get("c4")
     out = []
-    for ues in (236, 224, 200):
+    for ues in (249, 240, 232, 224):
         w = base.scaled(ues=ues)
         C, n = w.C, w.n_per_call
         steps_total = args.warmup + args.steps + 1

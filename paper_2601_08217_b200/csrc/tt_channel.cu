@@ -75,13 +75,13 @@ struct Plan {
 
 constexpr size_t kSmemBudget = 227 * 1024;  // one CTA per SM
 
-// must match tt_conv_kernel's layout: 128 B of barriers + `stages` x [win | coef | xo]
+// must match tt_conv_kernel's layout: 128 B of barriers + `stages` x [meta | win | coef | xo]
 // (L = taps per gain row: top-n when sparse, whose offsets come one row per interval)
 size_t smem_bytes(int R, int CW, int stages, int H, int L, int L4, int S, bool noise, bool xo_rows, int* nk_out) {
     const int T = CW * 32 * R;
     const int nk = (T - 1) / S + 2;  // worst-case intervals touched by a tile
     *nk_out = nk;
-    const size_t st = (static_cast<size_t>(H) + T) * 8 + static_cast<size_t>(nk) * L * 16 +
+    const size_t st = 16 + (static_cast<size_t>(H) + T + 2) * 8 + static_cast<size_t>(nk) * L * 16 +
                       static_cast<size_t>(xo_rows ? nk : 1) * L4 * 4;
     (void)noise;  // the noise variant needs no extra shared memory (fused epilogue)
     return 128 + static_cast<size_t>(stages) * st;
@@ -112,6 +112,7 @@ struct tt_channel_s {
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
     std::vector<int32_t> sorted_d;  // [C][L] delays in sorted-tap order (host; rebuilds the rw table)
     int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
+    bool force_robust = false;  // TT_ROBUST=1: the robust tiled variant for every call (tests)
     bool pdl = true;            // launch the tiled kernel with programmatic dependent launch (TT_PDL=0: off)
     int32_t top_n = 0;          // NEXT f2: taps kept per interval (0 = dense)
     int32_t n4 = 0;             // sparse offsets row stride (>= top_n + 1, multiple of 4)
@@ -137,11 +138,17 @@ namespace {
 
 template <int R, int CW, bool NOISE>
 cudaError_t prepare_kernel(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem));
+    const int sm = static_cast<int>(smem);
+    for (cudaError_t e : {cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false, false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                          cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                          cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                          cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, sm)})
+        if (e != cudaSuccess) return e;
+    return cudaSuccess;
 }
 
 // tile shapes (R outputs per thread, CW consumer warps), in order of preference
@@ -368,7 +375,17 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
                (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row || sparse)) {
         const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
         const int T = tp.CW * 32 * tp.R;
-        p.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
+        // a short lead-in tile when the call does not start on a 32R-aligned global
+        // sample (call lengths not a multiple of it), so the other tiles' warps keep the
+        // one-interval fast path and the paired noise draw
+        const int64_t A = 32 * tp.R;
+        p.lead = static_cast<int32_t>((A - h->t % A) % A);
+        if (p.lead >= n) p.lead = 0;
+        p.tiles_per_ch = static_cast<int32_t>(p.lead ? 1 + (n - p.lead + T - 1) / T : (n + T - 1) / T);
+        // the robust kernel variant (lead-in tile, window shift for input rows 8 B off a
+        // 16-B boundary) only when the call needs it; aligned calls run the plain schedule
+        const bool robust =
+            h->force_robust || p.lead != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0 || (n & 1) != 0;
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
         if (ar.agg) {
             // fused chunk sums: straight into agg when a group is one chunk, else into
@@ -403,15 +420,20 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-#define TT_LAUNCH(RR, CC)                                                                   \
-    do {                                                                                    \
-        if (noise) {                                                                        \
-            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, true, true>, p);   \
-            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, true, false>, p);      \
-        } else {                                                                            \
-            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, false, true>, p);  \
-            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, false, false>, p);     \
-        }                                                                                   \
+#define TT_LAUNCH_R(RR, CC, RB)                                                                 \
+    do {                                                                                        \
+        if (noise) {                                                                            \
+            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, true, true, RB>, p);   \
+            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, true, false, RB>, p);      \
+        } else {                                                                                \
+            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, false, true, RB>, p);  \
+            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<RR, CC, false, false, RB>, p);     \
+        }                                                                                       \
+    } while (0)
+#define TT_LAUNCH(RR, CC)                         \
+    do {                                          \
+        if (robust) TT_LAUNCH_R(RR, CC, true);    \
+        else TT_LAUNCH_R(RR, CC, false);          \
     } while (0)
         switch (tp.R * 100 + tp.CW) {
             case 816: TT_LAUNCH(8, 16); break;
@@ -421,6 +443,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
             default: TT_LAUNCH(2, 16); break;
         }
 #undef TT_LAUNCH
+#undef TT_LAUNCH_R
         if (ar.agg && nchunks > 1) {
             const int64_t tot = static_cast<int64_t>(ngroups) * n;
             const int64_t gg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);
@@ -552,6 +575,7 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     h->cap = snapshot_capacity;
     h->chan_off = channel_offset;
     if (const char* fp = getenv("TT_PDL")) h->pdl = atoi(fp) != 0;
+    if (const char* fr = getenv("TT_ROBUST")) h->force_robust = atoi(fr) != 0;
 
     // per channel: taps sorted by delay (stable: ties keep tap index order); perm[c][j]
     // is the original index of sorted tap j, xoff[c][j] its window offset H - d

@@ -66,6 +66,7 @@ struct ConvParams {
     int32_t t_mod;          // t % S
     int32_t c_lo;           // first channel of this launch
     int32_t tiles_per_ch;
+    int32_t lead;           // outputs in a short first tile that aligns the others (0 = none)
     int32_t L, L4, H, S;
     int32_t nk_max;         // max snapshot intervals a tile touches
     int32_t stages;         // shared-memory pipeline depth (<= kMaxStages)
@@ -212,14 +213,25 @@ struct TileWalk {
     }
 };
 
-template <int R, int CW>
+template <int R, int CW, bool ROBUST>
 __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int32_t c, int32_t tl) {
     constexpr int T = CW * 32 * R;
     TileInfo ti;
     ti.c = c;
-    ti.i0 = static_cast<int64_t>(tl) * T;
-    const int64_t rem = p.n - ti.i0;
-    ti.Tt = rem < T ? static_cast<int32_t>(rem) : T;
+    // with a lead-in (p.lead > 0) tile 0 is [0, lead) and tile tl >= 1 starts at
+    // lead + (tl - 1) T, a multiple of 32R in global samples: every warp then starts on a
+    // 32R-aligned sample (one snapshot interval per warp, paired noise) whatever the
+    // call lengths so far
+    if constexpr (ROBUST) {
+        const int64_t base = static_cast<int64_t>(tl) * T - (p.lead ? T - p.lead : 0);
+        ti.i0 = base < 0 ? 0 : base;
+        const int64_t end = base + T < p.n ? base + T : p.n;
+        ti.Tt = static_cast<int32_t>(end - ti.i0);
+    } else {
+        ti.i0 = static_cast<int64_t>(tl) * T;
+        const int64_t rem = p.n - ti.i0;
+        ti.Tt = rem < T ? static_cast<int32_t>(rem) : T;
+    }
     const uint32_t u0 = static_cast<uint32_t>(p.t_mod) + static_cast<uint32_t>(ti.i0);  // (t + i0) - (t / S) S
     const uint32_t q0 = div_S(p, u0);
     ti.kq = q0;
@@ -231,6 +243,7 @@ __device__ __forceinline__ TileInfo tile_info(const ConvParams& p, int32_t c, in
 // One pipeline stage in shared memory: input window (H + T float2), coefficient rows
 // (nk_max x L float4), tap offsets (L4 int32). Every region is a multiple of 16 B.
 struct Stage {
+    int32_t* meta;  // [0]: window shift (0 or 1 float2) chosen by the producer for this tile
     float2* win;
     float4* coef;
     int32_t* xo;
@@ -238,7 +251,7 @@ struct Stage {
 
 // Producer warp: stage tile `w` and arm `full` (plain parts first, then the barrier,
 // then the TMA bodies).
-template <int R>
+template <int R, bool ROBUST>
 __device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, uint64_t* full,
                                              int lane) {
     const int32_t H = p.H;
@@ -246,12 +259,18 @@ __device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo
     const int64_t hi = ti.i0 + ti.Tt;
     // A: delay-line history, call-local [lo, min(0, hi)) -> history index H + local
     const int64_t nA = lo < 0 ? ((hi < 0 ? hi : 0) - lo) : 0;
-    const Piece a = make_piece(st.win, p.hist_rd + static_cast<int64_t>(ti.c) * H + (H + lo),
-                               static_cast<uint32_t>(nA) * 8u);
     // B: this call's input, call-local [max(lo, 0), hi)
     const int64_t bl = lo < 0 ? 0 : lo;
     const int64_t row = p.in_row ? static_cast<int64_t>(__ldg(p.in_row + ti.c)) : static_cast<int64_t>(ti.c - p.c_lo);
-    const Piece bx = make_piece(st.win + (bl - lo), p.x + row * p.n + bl, static_cast<uint32_t>(hi - bl) * 8u);
+    const float2* xsrc = p.x + row * p.n + bl;
+    // the window starts one float2 later when the input row is 8 B off a 16-B boundary
+    // (odd call lengths), so that the large x piece stays a TMA copy (src and dst must
+    // agree mod 16); bl - lo is even, st.win is 16-B aligned
+    const int32_t wsh = ROBUST ? static_cast<int32_t>((reinterpret_cast<uintptr_t>(xsrc) >> 3) & 1u) : 0;
+    float2* const win = st.win + wsh;
+    const Piece a = make_piece(win, p.hist_rd + static_cast<int64_t>(ti.c) * H + (H + lo),
+                               static_cast<uint32_t>(nA) * 8u);
+    const Piece bx = make_piece(win + (bl - lo), xsrc, static_cast<uint32_t>(hi - bl) * 8u);
     // C, D: coefficient rows kb .. kb + nk - 1, wrapping at the ring's capacity
     const int64_t s0 = (p.t_div + ti.kq) % p.cap;
     const int32_t r1 = static_cast<int32_t>((p.cap - s0) < ti.nk ? (p.cap - s0) : ti.nk);
@@ -277,6 +296,7 @@ __device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo
     piece_plain(c2, lane);
     piece_plain(e, lane);
     piece_plain(f, lane);
+    if (ROBUST && lane == 0) *st.meta = wsh;
     __syncwarp();  // the lanes' plain stores happen-before lane 0's release (arrive)
     if (lane == 0) {
         mbar_arrive_expect_tx(full, a.body + bx.body + c1.body + c2.body + e.body + f.body);
@@ -516,7 +536,7 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
 }
 
 // CW consumer warps + 1 producer warp; tile T = CW x 32 x R outputs of one channel
-template <int R, int CW, bool NOISE, bool GEN>
+template <int R, int CW, bool NOISE, bool GEN, bool ROBUST>
 // (shapes with <= 8 consumer warps and R <= 8 run two CTAs per SM: independent CTAs drift apart, so
 // one CTA's noise epilogue can overlap the other's tap loop; measured slower, opt-in)
 __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt_conv_kernel(const ConvParams p) {
@@ -526,15 +546,22 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
     //   stage = [win (H+T) float2][coef nk_max x L float4][xo (sparse: nk_max x) L4 int32]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
-    const int64_t WB = static_cast<int64_t>(p.H + T) * 8;
+    // ROBUST: meta + window with one float2 of shift room; else the window alone
+    const int64_t WB = ROBUST ? 16 + static_cast<int64_t>(p.H + T + 2) * 8 : static_cast<int64_t>(p.H + T) * 8;
     const int64_t CB = static_cast<int64_t>(p.nk_max) * p.L * 16;
     const int64_t SB = WB + CB + static_cast<int64_t>(p.xoff_rows ? p.nk_max : 1) * p.L4 * 4;
     auto stage = [&](int s) {
         unsigned char* base = smem + 128 + s * SB;
         Stage st;
-        st.win = reinterpret_cast<float2*>(base);
+        st.meta = reinterpret_cast<int32_t*>(base);
+        st.win = reinterpret_cast<float2*>(base + (ROBUST ? 16 : 0));
         st.coef = reinterpret_cast<float4*>(base + WB);
         st.xo = reinterpret_cast<int32_t*>(base + WB + CB);
+        return st;
+    };
+    // consumer view of a full stage: the window as the producer placed it
+    auto shifted = [](Stage st) {
+        if constexpr (ROBUST) st.win += *st.meta;
         return st;
     };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -567,7 +594,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
             TileWalk tw(static_cast<uint32_t>(p.tiles_per_ch));
             for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, next(), tw.next()) {
                 if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
-                produce_tile<R>(p, tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl)),
+                produce_tile<R, ROBUST>(p, tile_info<R, CW, ROBUST>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl)),
                                 stage(s), &full[s], lane);
             }
         } else {
@@ -575,7 +602,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
                 const SuperInfo si = super_info(p, su);
                 for (int32_t k = 0; k < si.kcount; ++k, next()) {
                     if (kk > 0) mbar_wait(&empty[s], (kk - 1) & 1);
-                    produce_tile<R>(p, tile_info<R, CW>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
+                    produce_tile<R, ROBUST>(p, tile_info<R, CW, ROBUST>(p, si.c_first + k, si.tl), stage(s), &full[s], lane);
                 }
             }
         }
@@ -593,8 +620,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
             for (int64_t w = blockIdx.x; w < p.total_tiles; w += gridDim.x, next(), tw.next()) {
                 mbar_wait(&full[s], ph);
                 const TileInfo ti =
-                    tile_info<R, CW>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl));
-                consume_tile<R, CW, NOISE, GEN>(p, ti, stage(s), warp, lane, true, nullptr);
+                    tile_info<R, CW, ROBUST>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl));
+                consume_tile<R, CW, NOISE, GEN>(p, ti, shifted(stage(s)), warp, lane, true, nullptr);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
@@ -603,11 +630,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
                 const SuperInfo si = super_info(p, su);
                 for (int32_t k = 0; k < si.kcount; ++k, next()) {
                     mbar_wait(&full[s], ph);
-                    const TileInfo ti = tile_info<R, CW>(p, si.c_first + k, si.tl);
+                    const TileInfo ti = tile_info<R, CW, ROBUST>(p, si.c_first + k, si.tl);
                     // the chunk's sum goes straight into the group row, or into its partial row
                     float2* aggdst =
                         p.agg ? p.agg + (static_cast<int64_t>(si.g) * p.nchunks + si.q) * p.n + ti.i0 : nullptr;
-                    consume_tile<R, CW, NOISE, true>(p, ti, stage(s), warp, lane, k == 0, aggdst);
+                    consume_tile<R, CW, NOISE, true>(p, ti, shifted(stage(s)), warp, lane, k == 0, aggdst);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                 }

@@ -174,16 +174,23 @@ def test_error_codes(cuda_device):
     ("c4", dict(ues=1, n_per_call=12_000, calls=1, S=64), [100, 11_900]),   # warps off interval starts
 ])
 def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
-    """The register-window kernel (default for S % 16 == 0), the tiled kernel and the
-    generic kernel run the same per-output operation sequence: outputs are equal bit for
-    bit, for any call split (history carried across 16-misaligned call starts)."""
+    """The tiled kernel (default), its robust variant (lead-in tile and window shift, used
+    for calls that do not start on a 32R-aligned sample or rows off a 16-B boundary; forced
+    here with TT_ROBUST=1), the register-window kernels and the generic kernel run the
+    same per-output operation sequence: outputs are equal bit for bit, for any call split
+    (history carried across 16-misaligned call starts)."""
     w = ttsynth.get(name).scaled(**kw)
     run = Run(w, seed=21)
     outs = {}
     for k in ("rw", "rw8", "tiled", "generic"):
         monkeypatch.setenv("TT_KERNEL", k)
         outs[k] = run.gpu(cuda_device, calls=calls)
+    monkeypatch.setenv("TT_KERNEL", "tiled")
+    monkeypatch.setenv("TT_ROBUST", "1")
+    outs["robust"] = run.gpu(cuda_device, calls=calls)
+    monkeypatch.delenv("TT_ROBUST")
     monkeypatch.delenv("TT_KERNEL")
+    assert np.array_equal(outs["robust"], outs["tiled"])
     assert np.array_equal(outs["rw"], outs["tiled"])
     assert np.array_equal(outs["rw8"], outs["tiled"])
     assert np.array_equal(outs["rw"], outs["generic"])

@@ -247,6 +247,37 @@ def run_realtime(args, dev, peaks):
          {"higher_is_better": False, "per_ue_count": out})
 
 
+def run_align(args, dev, peaks):
+    """Robustness: c4 slot calls whose length is odd (61,441 samples) vs the even 61,440,
+    so odd channel rows start 8 B off a 16-B boundary and every other call starts on an
+    odd sample (odd-base noise path)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    out = []
+    for n in (61440, 61441):
+        w = ttsynth.get("c4").scaled(n_per_call=n)
+        C = w.C
+        steps_total = args.warmup + args.steps + 1
+        K = (steps_total * n - 1) // w.S + 2
+        P = min(steps_total, max(2, math.ceil(4 * bench.L2_BYTES / (C * n * 8))))
+        xs = [ttsynth.iq(w, 0, C, i, backend="torch", device=dev) for i in range(P)]
+        y = torch.empty_like(xs[0])
+        ch = Channel(ttsynth.delays(w), w.S, seed=1, snapshot_capacity=K, device=dev)
+        ch.load_snapshots(ttsynth.snapshots(w, 0, C, K, backend="torch", device=dev), 0)
+        torch.cuda.synchronize()
+        el, per, clk = timed(lambda i: ch.apply(xs[i % P], out=y, noise_sigma=w.sigma), args.steps, args.warmup,
+                             torch.cuda.current_stream())
+        ch.close()
+        del xs
+        torch.cuda.empty_cache()
+        out.append({"n_per_call": n, "ms_per_call": el / args.steps, "samples_per_s": C * n / (el / args.steps / 1e3)})
+    line("align", "c4 slot calls, odd vs even call length", out[1]["samples_per_s"], "samples/s", args.steps,
+         args.warmup, out[1]["ms_per_call"], [o["ms_per_call"] for o in out], clk,
+         {"workload": "c4 with 61,441-sample calls (odd) vs 61,440 (even)"}, {"per_length": out})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
@@ -260,7 +291,7 @@ def main():
     peaks = bench._peaks()
     for m in args.modes.split(","):
         {"aggregate": run_aggregate, "sparse": run_sparse, "links": run_links, "synth": run_synth,
-         "load": run_load, "realtime": run_realtime}[m](args, dev, peaks)
+         "load": run_load, "realtime": run_realtime, "align": run_align}[m](args, dev, peaks)
         torch.cuda.empty_cache()
 
 

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define TT_ABI_VERSION 1
+#define TT_ABI_VERSION 2
 #define TT_MAX_DELAY 4096  /* delays are integers in [0, TT_MAX_DELAY] (R5) */
 #define TT_MAX_TAPS 4096
 
@@ -81,6 +81,7 @@ typedef struct {
     int32_t launches_per_apply; /* kernel launches one tt_channel_apply enqueues */
     int32_t kernel;             /* TT_KERNEL_* the plan selected */
     int32_t top_n;              /* NEXT f2 taps per interval (0 = dense) */
+    int32_t device_clock;       /* 1 in device-clock mode (tt_channel_set_device_clock); t is then stale */
 } tt_channel_info;
 
 /* kernels a plan can select (all compute the same per-output operation sequence, so
@@ -206,6 +207,31 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
 /* t = 0 and zero delay-line history (stream-ordered on `stream`); the resident
  * snapshot range is kept. Errors: INVALID_ARG, CUDA. */
 tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream);
+
+/* Device-clock mode, for slot loops captured into a CUDA graph (SURVEY §7.3 item 6:
+ * "allow CUDA-Graph capture of slot loops").
+ *
+ * A kernel launch bakes its arguments, so a captured tt_channel_apply would replay the
+ * same stream position t and the same delay-line half. In device-clock mode the
+ * position and the history parity live in device memory instead. Each apply's kernel
+ * reads them after the previous grid has completed (programmatic dependent launch
+ * wait), and the last CTA to finish advances them by n_samples. A graph of K slot calls
+ * therefore replays the next K slots every time.
+ *
+ * enable = 1: stream-ordered on `stream`, copies the handle's (t, parity) to the device.
+ *   Requires the tiled kernel plan (else UNSUPPORTED) and t % A == 0, where A = 32R of
+ *   the plan (256 for the default tile). While enabled:
+ *   - tt_channel_apply and tt_channel_apply_aggregate need n_samples % A == 0 (else
+ *     UNSUPPORTED), so every call stays on the aligned fast path;
+ *   - snapshot residency is not checked per call: the caller keeps the ring loaded for
+ *     every slot a graph will replay;
+ *   - tt_channel_apply_host returns UNSUPPORTED;
+ *   - tt_channel_get_info reports device_clock = 1 and a stale t;
+ *   - tt_channel_reset also resets the device clock.
+ * enable = 0: synchronises `stream` and reads the device clock back into the handle's
+ *   t and parity (host-side validation resumes).
+ * Calling with the current mode is a no-op. Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
+tt_status tt_channel_set_device_clock(tt_channel_t h, int32_t enable, tt_stream_t stream);
 
 /* Fill *info. Errors: INVALID_ARG. */
 tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info);

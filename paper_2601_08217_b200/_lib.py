@@ -36,6 +36,7 @@ EXPORTS = (
     "tt_channel_apply_aggregate",
     "tt_synth_jakes",
     "tt_channel_reset",
+    "tt_channel_set_device_clock",
     "tt_channel_get_info",
     "tt_channel_destroy",
     "tt_last_error",
@@ -69,6 +70,7 @@ class ChannelInfo(ct.Structure):
         ("launches_per_apply", ct.c_int32),
         ("kernel", ct.c_int32),
         ("top_n", ct.c_int32),
+        ("device_clock", ct.c_int32),
     ]
 
 
@@ -99,11 +101,12 @@ def lib() -> ct.CDLL:
             L.tt_synth_jakes.argtypes = [P, P, i32, i32, i32, ct.c_double, u64, i64, i64, i64, P, P, P]
             L.tt_synth_jakes.restype = ct.c_int
             L.tt_channel_reset.argtypes = [P, P]
+            L.tt_channel_set_device_clock.argtypes = [P, i32, P]
             L.tt_channel_get_info.argtypes = [P, ct.POINTER(ChannelInfo)]
             L.tt_channel_destroy.argtypes = [P]
             for f in ("tt_channel_create", "tt_channel_load_snapshots", "tt_channel_apply", "tt_channel_apply_host",
                       "tt_channel_set_top_n",
-    "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset",
+    "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset", "tt_channel_set_device_clock",
                       "tt_channel_get_info", "tt_channel_destroy"):
                 getattr(L, f).restype = ct.c_int
             L.tt_last_error.argtypes = []
@@ -164,6 +167,10 @@ def tt_synth_jakes(delay_ptr: int, power_ptr: int, num_ue: int, num_paths: int, 
 
 def tt_channel_reset(h: int, stream: int) -> None:
     check(lib().tt_channel_reset(h, stream))
+
+
+def tt_channel_set_device_clock(h: int, enable: bool, stream: int) -> None:
+    check(lib().tt_channel_set_device_clock(h, 1 if enable else 0, stream))
 
 
 def tt_channel_get_info(h: int) -> ChannelInfo:

@@ -165,6 +165,12 @@ class Channel:
     def reset(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         _lib.tt_channel_reset(self.handle, _stream_ptr(stream))
 
+    def set_device_clock(self, enable: bool, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Device-clock mode (tt_channel_set_device_clock): the stream position lives on
+        the GPU, so slot calls can be captured into a CUDA graph and replayed; calls
+        then need n % 256 == 0 and snapshot residency is the caller's contract."""
+        _lib.tt_channel_set_device_clock(self.handle, enable, _stream_ptr(stream))
+
 
 def synth_jakes(path_delay, path_power, num_sinusoids: int, nu: float, seed: int, first_index: int, count: int,
                 channel_offset: int = 0, device=None, stream: Optional[torch.cuda.Stream] = None):

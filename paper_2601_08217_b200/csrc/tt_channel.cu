@@ -112,6 +112,8 @@ struct tt_channel_s {
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
     std::vector<int32_t> sorted_d;  // [C][L] delays in sorted-tap order (host; rebuilds the rw table)
     int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
+    tt::DevClock* dclk = nullptr;  // device clock (stream position for graph-captured slot loops)
+    bool dclock = false;           // tt_channel_set_device_clock: kernels run on dclk
     bool force_robust = false;  // TT_ROBUST=1: the robust tiled variant for every call (tests)
     bool pdl = true;            // launch the tiled kernel with programmatic dependent launch (TT_PDL=0: off)
     int32_t top_n = 0;          // NEXT f2: taps kept per interval (0 = dense)
@@ -341,6 +343,8 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     const size_t hs = static_cast<size_t>(h->C) * h->H;
     p.hist_rd = h->hist + h->p * hs;
     p.hist_wr = h->hist + (1 - h->p) * hs;
+    p.hist_base = h->hist;
+    p.hist_half = static_cast<int64_t>(hs);
     const bool sparse = h->top_n > 0;
     p.ring = sparse ? h->sring : h->ring;
     p.xoff = h->xoff;
@@ -379,13 +383,14 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         // sample (call lengths not a multiple of it), so the other tiles' warps keep the
         // one-interval fast path and the paired noise draw
         const int64_t A = 32 * tp.R;
-        p.lead = static_cast<int32_t>((A - h->t % A) % A);
+        p.lead = h->dclock ? 0 : static_cast<int32_t>((A - h->t % A) % A);  // device clock: aligned by contract
         if (p.lead >= n) p.lead = 0;
         p.tiles_per_ch = static_cast<int32_t>(p.lead ? 1 + (n - p.lead + T - 1) / T : (n + T - 1) / T);
         // the robust kernel variant (lead-in tile, window shift for input rows 8 B off a
         // 16-B boundary) only when the call needs it; aligned calls run the plain schedule
-        const bool robust =
-            h->force_robust || p.lead != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0 || (n & 1) != 0;
+        const bool robust = h->dclock || h->force_robust || p.lead != 0 ||
+                            (reinterpret_cast<uintptr_t>(x) & 15u) != 0 || (n & 1) != 0;
+        if (h->dclock) p.clk = h->dclk;
         p.total_tiles = static_cast<int64_t>(nch) * p.tiles_per_ch;
         if (ar.agg) {
             // fused chunk sums: straight into agg when a group is one chunk, else into
@@ -477,6 +482,11 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     return TT_OK;
 }
 
+// alignment the device-clock mode keeps every call start on (32R of the tiled plans)
+int64_t clock_grid(const tt_channel_s* h) {
+    return 32 * std::max(h->plan.tiled[0].R, h->plan.tiled[1].R);
+}
+
 tt_status check_apply(tt_channel_s* h, const void* in, const void* out, int64_t n, float sigma) {
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
     if (!in || !out) return fail(TT_ERR_INVALID_ARG, "NULL in/out");
@@ -484,6 +494,15 @@ tt_status check_apply(tt_channel_s* h, const void* in, const void* out, int64_t 
     if (n > (int64_t(1) << 30)) return fail(TT_ERR_INVALID_ARG, "n_samples must be <= 2^30 per call (got %lld)", (long long)n);
     if (in == out) return fail(TT_ERR_INVALID_ARG, "in and out must not overlap");
     if (!(sigma >= 0.0f) || !std::isfinite(sigma)) return fail(TT_ERR_INVALID_ARG, "noise_sigma must be finite and >= 0");
+    if (h->dclock) {
+        // the stream position lives on the device: calls must keep it on the 32R grid,
+        // and snapshot residency is the caller's contract (not checked per call)
+        const int64_t A = clock_grid(h);
+        if (n % A != 0)
+            return fail(TT_ERR_UNSUPPORTED, "device-clock mode needs n_samples %% %lld == 0 (got %lld)", (long long)A,
+                        (long long)n);
+        return TT_OK;
+    }
     const int64_t k_lo = h->t / h->S;
     const int64_t k_hi = (h->t + n - 1) / h->S + 1;
     if (h->res_hi <= h->res_lo || k_lo < h->res_lo || k_hi >= h->res_hi)
@@ -498,6 +517,7 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->perm);
     cudaFree(h->xoff);
     cudaFree(h->tab);
+    cudaFree(h->dclk);
     cudaFree(h->in_row);
     cudaFree(h->sring);
     cudaFree(h->soff);
@@ -607,6 +627,8 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     if ((e = cudaMalloc(&h->perm, pm_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
     if ((e = cudaMalloc(&h->xoff, xo_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(xoff)"));
     if ((e = cudaMalloc(&h->tab, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(tab)"));
+    if ((e = cudaMalloc(&h->dclk, sizeof(tt::DevClock))) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(clock)"));
+    if ((e = cudaMemset(h->dclk, 0, sizeof(tt::DevClock))) != cudaSuccess) return bail(cuda_fail(e, "zero clock"));
     h->dev_bytes = ring_b + hist_b + pm_b + xo_b + tb_b;
     if ((e = cudaMemset(h->tab, 0, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "zero tab"));
     if ((e = cudaMemcpy(h->perm, pm.data(), pm_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
@@ -697,13 +719,16 @@ tt_status tt_channel_apply(tt_channel_t h, const float* in, float* out, int64_t 
     s = launch(h, reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), 0, h->C, n_samples,
                noise_sigma, static_cast<cudaStream_t>(stream));
     if (s != TT_OK) return s;
-    h->t += n_samples;
-    if (h->H > 0) h->p ^= 1;
+    if (!h->dclock) {
+        h->t += n_samples;
+        if (h->H > 0) h->p ^= 1;
+    }
     return TT_OK;
 }
 
 tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                                 tt_stream_t stream) {
+    if (h && h->dclock) return fail(TT_ERR_UNSUPPORTED, "apply_host in device-clock mode: use tt_channel_apply");
     tt_status s = check_apply(h, in, out, n_samples, noise_sigma);
     if (s != TT_OK) return s;
     if (h->in_row) return fail(TT_ERR_UNSUPPORTED, "apply_host with an input map: use tt_channel_apply");
@@ -874,8 +899,10 @@ tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out
     s = launch(h, reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), 0, h->C, n_samples,
                noise_sigma, static_cast<cudaStream_t>(stream), ar);
     if (s != TT_OK) return s;
-    h->t += n_samples;
-    if (h->H > 0) h->p ^= 1;
+    if (!h->dclock) {
+        h->t += n_samples;
+        if (h->H > 0) h->p ^= 1;
+    }
     return TT_OK;
 }
 
@@ -954,6 +981,35 @@ tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream) {
                 "zero history");
     h->t = 0;
     h->p = 0;
+    if (h->dclock) {
+        tt::tt_set_clock_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(h->dclk, 0, 0);
+        TT_CUDA(cudaGetLastError(), "reset clock");
+    }
+    return TT_OK;
+}
+
+tt_status tt_channel_set_device_clock(tt_channel_t h, int32_t enable, tt_stream_t stream) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    DeviceGuard dg(h->dev);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (enable && !h->dclock) {
+        if (h->plan.kind != TT_KERNEL_TILED || h->plan.tiled[0].R == 0 || h->plan.tiled[1].R == 0)
+            return fail(TT_ERR_UNSUPPORTED, "device-clock mode needs the tiled kernel for this handle's shape");
+        const int64_t A = clock_grid(h);
+        if (h->t % A != 0)
+            return fail(TT_ERR_UNSUPPORTED, "device-clock mode must start at t %% %lld == 0 (t = %lld)", (long long)A,
+                        (long long)h->t);
+        tt::tt_set_clock_kernel<<<1, 1, 0, st>>>(h->dclk, h->t, h->p);
+        TT_CUDA(cudaGetLastError(), "set clock");
+        h->dclock = true;
+    } else if (!enable && h->dclock) {
+        tt::DevClock c{};
+        TT_CUDA(cudaStreamSynchronize(st), "clock sync");
+        TT_CUDA(cudaMemcpy(&c, h->dclk, sizeof(c), cudaMemcpyDeviceToHost), "read clock");
+        h->t = c.t;
+        h->p = c.par;
+        h->dclock = false;
+    }
     return TT_OK;
 }
 
@@ -976,6 +1032,7 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
                                               h->agg_scratch_elems * sizeof(float2));
     info->kernel = h->plan.kind;
     info->top_n = h->top_n;
+    info->device_clock = h->dclock ? 1 : 0;
     info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? h->plan.rw_R
                                : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R : 0;
     info->launches_per_apply = h->plan.kind == TT_KERNEL_GENERIC ? 2 : 1;

@@ -42,6 +42,15 @@ constexpr int kConsumerWarps = 16;                   // default tile shape: 16 c
 constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
 constexpr int kMaxStages = 4;
 
+// Stream position kept in device memory (tt_channel_set_device_clock): the kernel
+// reads t and the history parity at its start and its last CTA advances them, so a
+// captured CUDA graph of slot calls replays correctly.
+struct DevClock {
+    int64_t t;      // global index of the next call's first sample
+    int32_t par;    // history buffer holding the current delay line
+    uint32_t done;  // CTAs of the running call that have finished (last one advances)
+};
+
 struct ConvParams {
     const float2* x;        // [rows][n]: row of channel c = in_row ? in_row[c] : c - c_lo
     float2* y;              // [C_launch][n] per-channel outputs, or nullptr (aggregate only)
@@ -74,6 +83,9 @@ struct ConvParams {
     float noise_sc;         // sigma / sqrt(2) as float; 0 = no noise
     int32_t s_shift;        // log2(S) if S is a power of two, else -1
     float inv_S;            // 1/S (exact when S is a power of two)
+    DevClock* clk;          // device clock (ROBUST variant only), or nullptr: t/history from above
+    float2* hist_base;      // [2][C][H] history ping-pong (device-clock mode picks the half)
+    int64_t hist_half;      // C * H
 };
 
 // ---------------------------------------------------------------------------------
@@ -539,7 +551,7 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
 template <int R, int CW, bool NOISE, bool GEN, bool ROBUST>
 // (shapes with <= 8 consumer warps and R <= 8 run two CTAs per SM: independent CTAs drift apart, so
 // one CTA's noise epilogue can overlap the other's tap loop; measured slower, opt-in)
-__global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt_conv_kernel(const ConvParams p) {
+__device__ __forceinline__ void conv_body(const ConvParams& p) {
     constexpr int T = CW * 32 * R;
     extern __shared__ __align__(128) unsigned char smem[];
     // layout: [full kMaxStages x 8 B | empty kMaxStages x 8 B | pad to 128][stage 0][stage 1]...
@@ -643,6 +655,43 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
     }
 }
 
+// The tiled kernel. The ROBUST variant can run on the device clock: it waits for the
+// previous grid (PDL) before reading it, and the last CTA to finish advances it.
+template <int R, int CW, bool NOISE, bool GEN, bool ROBUST>
+__global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt_conv_kernel(const ConvParams p) {
+    if constexpr (ROBUST) {
+        ConvParams q = p;
+        int64_t t = 0;
+        int32_t par = 0;
+        if (p.clk) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            t = *reinterpret_cast<volatile int64_t*>(&p.clk->t);
+            par = *reinterpret_cast<volatile int32_t*>(&p.clk->par);
+            q.t = t;
+            q.t_div = p.s_shift >= 0 ? (t >> p.s_shift) : t / p.S;
+            q.t_mod = static_cast<int32_t>(t - q.t_div * p.S);
+            q.hist_rd = p.hist_base + par * p.hist_half;
+            q.hist_wr = p.hist_base + (par ^ 1) * p.hist_half;
+        }
+        conv_body<R, CW, NOISE, GEN, ROBUST>(q);
+        if (p.clk) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(&p.clk->done, 1u) == gridDim.x - 1) {
+                    p.clk->t = t + p.n;
+                    p.clk->par = p.H > 0 ? (par ^ 1) : par;
+                    p.clk->done = 0u;
+                    __threadfence();
+                }
+            }
+        }
+    } else {
+        conv_body<R, CW, NOISE, GEN, ROBUST>(p);
+    }
+}
+
+
 // Generic path: one thread per output, operands straight from global memory. Used
 // when the tiled kernel's shared-memory plan does not fit (very long filters with very
 // short snapshot periods). Same per-output operation sequence => bit-identical.
@@ -688,6 +737,13 @@ __global__ void __launch_bounds__(256) tt_conv_generic_kernel(const ConvParams p
 
 // History update for the generic path (the tiled kernel fuses it): the new history is
 // the last H samples of (old history ++ x).
+// device clock := (t, par) (tt_channel_set_device_clock, reset)
+__global__ void tt_set_clock_kernel(DevClock* clk, int64_t t, int32_t par) {
+    clk->t = t;
+    clk->par = par;
+    clk->done = 0u;
+}
+
 __global__ void tt_history_kernel(const ConvParams p, int32_t nch) {
     const int64_t tot = static_cast<int64_t>(nch) * p.H;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;

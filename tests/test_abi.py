@@ -53,7 +53,7 @@ def test_library_is_sm100a():
 
 
 def test_version_and_status_strings(tt):
-    assert tt.tt_abi_version() == 1
+    assert tt.tt_abi_version() == 2
     L = tt.lib()
     assert L.tt_status_string(0) == b"TT_OK"
     assert L.tt_status_string(4) == b"TT_ERR_SNAPSHOT_MISSING"

@@ -283,3 +283,48 @@ def test_random_instances_vs_oracle(cuda_device):
         if np.abs(ref).max() > 0:
             compare(outs[0], ref, f"instance {inst}: C={C} L={L} D={D} S={S} N={N}")
     assert len(kinds) >= 3, kinds  # several plans were exercised
+
+
+def test_device_clock_cuda_graph_replay(cuda_device):
+    """slot calls captured into a CUDA graph replay the next slots
+    (device-clock mode: t and the delay-line half live on the GPU), bit-identical to
+    eager calls, and the clock reads back into the handle."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel, TTError
+
+    n, calls, per_graph = 4_096, 6, 2
+    w = ttsynth.get("c4").scaled(ues=3, n_per_call=n, calls=calls)
+    run = Run(w, seed=77)
+    eager = run.gpu(cuda_device)
+    compare(eager, run.oracle(), "device clock (eager reference)")
+
+    ch = Channel(run.delays, w.S, seed=run.seed, snapshot_capacity=run.K, device=cuda_device)
+    try:
+        ch.load_snapshots(torch.from_numpy(run.gains).to(cuda_device), 0)
+        ch.set_device_clock(True)
+        assert ch.info().device_clock == 1
+        xs = [torch.zeros((run.C, n, 2), dtype=torch.float32, device=cuda_device) for _ in range(per_graph)]
+        ys = [torch.zeros_like(x) for x in xs]
+        with pytest.raises(TTError, match="UNSUPPORTED"):
+            ch.apply(xs[0][:, :100].contiguous(), noise_sigma=run.sigma)  # n % 256 != 0
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for k in range(per_graph):
+                ch.apply(xs[k], out=ys[k], noise_sigma=run.sigma)
+        out = np.empty_like(eager)
+        for r in range(calls // per_graph):
+            for k in range(per_graph):
+                c = r * per_graph + k
+                xs[k].copy_(torch.from_numpy(np.ascontiguousarray(run.x[:, c * n:(c + 1) * n])))
+            g.replay()
+            torch.cuda.synchronize()
+            for k in range(per_graph):
+                c = r * per_graph + k
+                out[:, c * n:(c + 1) * n] = ys[k].cpu().numpy()
+        assert np.array_equal(out, eager)
+        ch.set_device_clock(False)
+        assert ch.t == calls * n and ch.info().device_clock == 0
+    finally:
+        ch.close()

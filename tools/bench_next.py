@@ -278,6 +278,49 @@ def run_align(args, dev, peaks):
          {"workload": "c4 with 61,441-sample calls (odd) vs 61,440 (even)"}, {"per_length": out})
 
 
+def run_graph(args, dev, peaks):
+    """slot loops eager vs captured into one CUDA graph of G calls
+    (device-clock mode) for the short-call configs c3 and c1; ms per call, device-timed."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    G = 10
+    res = []
+    for name in ("c3", "c1"):
+        w = ttsynth.get(name)
+        n = w.n_per_call if w.n_per_call % 256 == 0 else (w.n_per_call // 256) * 256
+        w = w.scaled(n_per_call=n)
+        C = w.C
+        reps = max(1, args.steps // G)
+        steps_total = (args.warmup + reps + 2) * G * 2 + 1
+        K = (steps_total * n - 1) // w.S + 2
+        xs = [ttsynth.iq(w, 0, C, i, backend="torch", device=dev) for i in range(G)]
+        ys = [torch.empty_like(x) for x in xs]
+        ch = Channel(ttsynth.delays(w), w.S, seed=1, snapshot_capacity=K, device=dev)
+        ch.load_snapshots(ttsynth.snapshots(w, 0, C, K, backend="torch", device=dev), 0)
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        el_e, per_e, clk = timed(lambda i: ch.apply(xs[i % G], out=ys[i % G], noise_sigma=w.sigma), reps * G,
+                                 args.warmup * G, st)
+        ch.set_device_clock(True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for k in range(G):
+                ch.apply(xs[k], out=ys[k], noise_sigma=w.sigma)
+        el_g, per_g, _ = timed(lambda i: g.replay(), reps, args.warmup, st)
+        ch.set_device_clock(False)
+        ch.close()
+        res.append({"config": name, "channels": C, "samples_per_call": n, "calls_per_graph": G,
+                    "eager_ms_per_call": el_e / (reps * G), "graph_ms_per_call": el_g / (reps * G),
+                    "speedup": (el_e / (reps * G)) / (el_g / (reps * G))})
+        del xs, ys
+        torch.cuda.empty_cache()
+    line("graph", "slot calls per s, eager vs CUDA graph (device clock)", 1e3 / res[0]["graph_ms_per_call"],
+         "calls/s", args.steps, args.warmup, res[0]["graph_ms_per_call"], [r["graph_ms_per_call"] for r in res], clk,
+         {"workload": "c3 and c1 slot loops, 10 calls per graph"}, {"per_config": res})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
@@ -291,7 +334,8 @@ def main():
     peaks = bench._peaks()
     for m in args.modes.split(","):
         {"aggregate": run_aggregate, "sparse": run_sparse, "links": run_links, "synth": run_synth,
-         "load": run_load, "realtime": run_realtime, "align": run_align}[m](args, dev, peaks)
+         "load": run_load, "realtime": run_realtime, "align": run_align,
+         "graph": run_graph}[m](args, dev, peaks)
         torch.cuda.empty_cache()
 
 

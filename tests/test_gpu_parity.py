@@ -117,6 +117,15 @@ def test_host_buffer_path_equals_device_path(cuda_device):
     assert np.array_equal(run.gpu(cuda_device, host_path=True), run.gpu(cuda_device))
 
 
+def test_host_buffer_path_many_chunks(cuda_device, monkeypatch):
+    """128 channels in 1 MiB chunks (32 channels each): the host path cycles its four
+    staging buffers and both copy-stream pairs; equal to the device path bit for bit."""
+    monkeypatch.setenv("TT_HOST_CHUNK_MB", "1")
+    w = ttsynth.get("c3").scaled(ues=64, n_per_call=4_096, calls=2)
+    run = Run(w, seed=8)
+    assert np.array_equal(run.gpu(cuda_device, host_path=True), run.gpu(cuda_device))
+
+
 def test_snapshot_ring_streaming(cuda_device):
     """A ring smaller than the run, refilled slot by slot (as a streaming user would)."""
     import torch

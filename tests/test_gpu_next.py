@@ -33,7 +33,7 @@ def _chunked_sum_f32(y, G):
     return out
 
 
-def _run_aggregate(run, device, G, calls, rows=None, x_rows=None, with_out=True):
+def _run_aggregate(run, device, G, calls, rows=None, x_rows=None, with_out=True, device_clock=False):
     import torch
 
     from paper_2601_08217_b200 import Channel
@@ -41,6 +41,8 @@ def _run_aggregate(run, device, G, calls, rows=None, x_rows=None, with_out=True)
     ch = Channel(run.delays, run.w.S, seed=run.seed, snapshot_capacity=run.K, channel_offset=run.c_lo, device=device)
     try:
         ch.load_snapshots(torch.from_numpy(run.gains).to(device), 0)
+        if device_clock:
+            ch.set_device_clock(True)
         src = run.x if x_rows is None else x_rows
         if rows is not None:
             ch.set_input_map(rows, src.shape[0])
@@ -84,6 +86,27 @@ def test_aggregation_streaming_and_kernel_paths_bit_identical(cuda_device, monke
     monkeypatch.delenv("TT_KERNEL")
     assert np.array_equal(one, gen)
     compare(one, oracle.aggregate(run.oracle(), 24), "c4 UL aggregate")
+
+
+def test_aggregation_and_links_in_device_clock_mode(cuda_device):
+    """Device-clock mode (the graph-capturable stream position) gives the same per-channel
+    outputs and group sums as host-clock calls, for the f1 aggregate and the f4 links."""
+    w = ttsynth.get("c4").scaled(ues=12, dirs=2, n_per_call=4_096, calls=3)
+    run = Run(w, seed=15)
+    calls = [4_096] * 3
+    y0, a0 = _run_aggregate(run, cuda_device, 24, calls)
+    y1, a1 = _run_aggregate(run, cuda_device, 24, calls, device_clock=True)
+    assert np.array_equal(y0, y1) and np.array_equal(a0, a1)
+    U, B = 4, 3
+    wl = ttsynth.get("c3").scaled(ues=U * B, dirs=1, n_per_call=2_048, calls=2)
+    rl = Run(wl, seed=16)
+    xg = ttsynth.iq(wl, 0, B, 0, 4_096)
+    rows = np.tile(np.arange(B, dtype=np.int32), U)
+    rl.x = xg[rows]
+    y0, a0 = _run_aggregate(rl, cuda_device, B, [2_048, 2_048], rows=rows, x_rows=xg)
+    y1, a1 = _run_aggregate(rl, cuda_device, B, [2_048, 2_048], rows=rows, x_rows=xg, device_clock=True)
+    assert np.array_equal(y0, y1) and np.array_equal(a0, a1)
+    compare(y0, rl.oracle(), "links")
 
 
 def test_multi_gnb_links(cuda_device):

@@ -204,8 +204,10 @@ tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32
 tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int64_t n_samples, float noise_sigma,
                                 tt_stream_t stream);
 
-/* t = 0 and zero delay-line history (stream-ordered on `stream`); the resident
- * snapshot range is kept. Errors: INVALID_ARG, CUDA. */
+/* t = 0 and zero delay-line history; the resident snapshot range is kept. No device
+ * work: calls at t = 0 read the delay line from a zero buffer (`stream` is used only in
+ * device-clock mode, where the device clock is reset stream-ordered on it).
+ * Errors: INVALID_ARG, CUDA. */
 tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream);
 
 /* Device-clock mode, for slot loops captured into a CUDA graph (SURVEY §7.3 item 6:

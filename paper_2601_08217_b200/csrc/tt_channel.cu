@@ -107,6 +107,7 @@ struct tt_channel_s {
     int64_t res_lo = 0, res_hi = 0;
     float4* ring = nullptr;    // [C][cap][L] (g_k, g_{k+1} - g_k), taps sorted by delay
     float2* hist = nullptr;    // [2][C][H] delay-line ping-pong
+    float2* hist_zero = nullptr;  // [C][H] zeros: the delay line at t = 0 (reset needs no device work)
     int32_t* perm = nullptr;   // [C][L] original tap index of sorted tap j
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
@@ -341,9 +342,12 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     const int32_t KC = ar.agg ? std::min<int32_t>(ar.G, TT_AGG_CHUNK) : 1;
     const int32_t nchunks = ar.agg ? (ar.G + KC - 1) / KC : 1;
     const size_t hs = static_cast<size_t>(h->C) * h->H;
-    p.hist_rd = h->hist + h->p * hs;
+    // at t = 0 the delay line is zero by definition: read the zero buffer, so a
+    // reset needs no device work
+    p.hist_rd = h->t == 0 ? h->hist_zero : h->hist + h->p * hs;
     p.hist_wr = h->hist + (1 - h->p) * hs;
     p.hist_base = h->hist;
+    p.hist_zero = h->hist_zero;
     p.hist_half = static_cast<int64_t>(hs);
     const bool sparse = h->top_n > 0;
     p.ring = sparse ? h->sring : h->ring;
@@ -514,6 +518,7 @@ tt_status check_apply(tt_channel_s* h, const void* in, const void* out, int64_t 
 void free_all(tt_channel_s* h) {
     cudaFree(h->ring);
     cudaFree(h->hist);
+    cudaFree(h->hist_zero);
     cudaFree(h->perm);
     cudaFree(h->xoff);
     cudaFree(h->tab);
@@ -624,16 +629,20 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     const size_t pm_b = pm.size() * sizeof(int32_t), xo_b = xo.size() * sizeof(int32_t);
     if ((e = cudaMalloc(&h->ring, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(snapshot ring)"));
     if (hist_b && (e = cudaMalloc(&h->hist, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(history)"));
+    if (hist_b && (e = cudaMalloc(&h->hist_zero, hist_b / 2)) != cudaSuccess)
+        return bail(cuda_fail(e, "cudaMalloc(zero history)"));
     if ((e = cudaMalloc(&h->perm, pm_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
     if ((e = cudaMalloc(&h->xoff, xo_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(xoff)"));
     if ((e = cudaMalloc(&h->tab, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(tab)"));
     if ((e = cudaMalloc(&h->dclk, sizeof(tt::DevClock))) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(clock)"));
     if ((e = cudaMemset(h->dclk, 0, sizeof(tt::DevClock))) != cudaSuccess) return bail(cuda_fail(e, "zero clock"));
-    h->dev_bytes = ring_b + hist_b + pm_b + xo_b + tb_b;
+    h->dev_bytes = ring_b + hist_b + hist_b / 2 + pm_b + xo_b + tb_b;
     if ((e = cudaMemset(h->tab, 0, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "zero tab"));
     if ((e = cudaMemcpy(h->perm, pm.data(), pm_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
     if ((e = cudaMemcpy(h->xoff, xo.data(), xo_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy xoff"));
     if (hist_b && (e = cudaMemset(h->hist, 0, hist_b)) != cudaSuccess) return bail(cuda_fail(e, "zero history"));
+    if (hist_b && (e = cudaMemset(h->hist_zero, 0, hist_b / 2)) != cudaSuccess)
+        return bail(cuda_fail(e, "zero history"));
     // the ring is zeroed so a never-loaded slot can never inject NaN into a CTA's
     // table (apply refuses non-resident ranges anyway)
     if ((e = cudaMemset(h->ring, 0, ring_b)) != cudaSuccess) return bail(cuda_fail(e, "zero ring"));
@@ -975,10 +984,7 @@ tt_status tt_synth_jakes(const float* path_delay, const float* path_power, int32
 tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream) {
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
     DeviceGuard dg(h->dev);
-    if (h->hist)
-        TT_CUDA(cudaMemsetAsync(h->hist, 0, 2 * static_cast<size_t>(h->C) * h->H * sizeof(float2),
-                                static_cast<cudaStream_t>(stream)),
-                "zero history");
+    // no device work for the delay line: calls at t = 0 read the zero buffer
     h->t = 0;
     h->p = 0;
     if (h->dclock) {

@@ -85,6 +85,7 @@ struct ConvParams {
     float inv_S;            // 1/S (exact when S is a power of two)
     DevClock* clk;          // device clock (ROBUST variant only), or nullptr: t/history from above
     float2* hist_base;      // [2][C][H] history ping-pong (device-clock mode picks the half)
+    const float2* hist_zero;  // [C][H] zeros, the delay line at t = 0
     int64_t hist_half;      // C * H
 };
 
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
             q.t = t;
             q.t_div = p.s_shift >= 0 ? (t >> p.s_shift) : t / p.S;
             q.t_mod = static_cast<int32_t>(t - q.t_div * p.S);
-            q.hist_rd = p.hist_base + par * p.hist_half;
+            q.hist_rd = t == 0 ? p.hist_zero : p.hist_base + par * p.hist_half;
             q.hist_wr = p.hist_base + (par ^ 1) * p.hist_half;
         }
         conv_body<R, CW, NOISE, GEN, ROBUST>(q);

@@ -497,10 +497,28 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
                     const uint32_t v0 = __shfl_xor_sync(0xffffffffu, s0, 1);
                     const uint32_t v1 = __shfl_xor_sync(0xffffffffu, s1, 1);
                     // select the words first so each lane runs the transform once per sample
-                    const float2 wa = noise_from_words(ev ? q.a : v0, ev ? q.b : v1, p.noise_sc);
-                    const float2 wb = noise_from_words(ev ? v0 : q.c, ev ? v1 : q.d, p.noise_sc);
+                    float2 wa, wb;
+                    noise_from_words2(ev ? q.a : v0, ev ? q.b : v1, ev ? v0 : q.c, ev ? v1 : q.d, p.noise_sc, wa,
+                                      wb);
                     out[r] = make_float2(__fadd_rn(out[r].x, wa.x), __fadd_rn(out[r].y, wa.y));
                     out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, wb.x), __fadd_rn(out[r + 1].y, wb.y));
+                }
+            } else if constexpr (R % 2 == 0) {
+                // odd tile base: every lane draws its own pair per row (rows two at a time)
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const int64_t n0 = nb + r * 32, n1 = n0 + 32;
+                    const uint64_t m0 = static_cast<uint64_t>(n0) >> 1, m1 = static_cast<uint64_t>(n1) >> 1;
+                    const u32x4 q0 = philox4x32_10(static_cast<uint32_t>(m0), static_cast<uint32_t>(m0 >> 32), cg, 0u,
+                                                   p.key0, p.key1);
+                    const u32x4 q1 = philox4x32_10(static_cast<uint32_t>(m1), static_cast<uint32_t>(m1 >> 32), cg, 0u,
+                                                   p.key0, p.key1);
+                    const bool odd = (n0 & 1) != 0;  // rows are 32 apart: same parity
+                    float2 w0, w1;
+                    noise_from_words2(odd ? q0.c : q0.a, odd ? q0.d : q0.b, odd ? q1.c : q1.a, odd ? q1.d : q1.b,
+                                      p.noise_sc, w0, w1);
+                    out[r] = make_float2(__fadd_rn(out[r].x, w0.x), __fadd_rn(out[r].y, w0.y));
+                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, w1.x), __fadd_rn(out[r + 1].y, w1.y));
                 }
             } else {
 #pragma unroll

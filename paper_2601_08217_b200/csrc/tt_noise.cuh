@@ -100,4 +100,73 @@ __device__ __forceinline__ float2 noise_from_words(uint32_t a, uint32_t b, float
     return make_float2(__fmul_rn(__fmul_rn(rho, ct), sc), __fmul_rn(__fmul_rn(rho, st), sc));
 }
 
+// Two samples at once, (a0, b0) and (a1, b1): the same operation sequence as
+// noise_from_words on each, with the floating-point steps packed into FFMA2 / FMUL2 /
+// FADD2 (per component exactly __fmaf_rn / __fmul_rn / __fadd_rn, so the results are
+// bit-identical) to halve their issue slots.
+__device__ __forceinline__ void noise_from_words2(uint32_t a0, uint32_t b0, uint32_t a1, uint32_t b1, float sc,
+                                                  float2& w0, float2& w1) {
+    // radius: rho = sqrt(-2 ln u), u = ((a >> 8) + 1) 2^-24
+    const uint32_t A0 = (a0 >> 8) + 1u, A1 = (a1 >> 8) + 1u;
+    const int e0 = 31 - __clz(A0), e1 = 31 - __clz(A1);
+    float2 m = __fmul2_rn(make_float2(__uint2float_rn(A0), __uint2float_rn(A1)),
+                          make_float2(__int_as_float((127 - e0) << 23), __int_as_float((127 - e1) << 23)));
+    const bool h0 = m.x > 0x1.6a09e6p+0f, h1 = m.y > 0x1.6a09e6p+0f;
+    const float2 mh = __fmul2_rn(m, make_float2(0.5f, 0.5f));
+    m = make_float2(h0 ? mh.x : m.x, h1 ? mh.y : m.y);
+    const int E0 = e0 - 24 + (h0 ? 1 : 0), E1 = e1 - 24 + (h1 ? 1 : 0);
+    const float2 f = __fadd2_rn(m, make_float2(-1.0f, -1.0f));  // fsub_rn(m, 1) == fadd_rn(m, -1)
+    auto c2 = [](float c) { return make_float2(c, c); };
+    float2 q = c2(-0x1.321a4cp-4f);
+    q = __ffma2_rn(q, f, c2(0x1.068b2ap-3f));
+    q = __ffma2_rn(q, f, c2(-0x1.0f9b0cp-3f));
+    q = __ffma2_rn(q, f, c2(0x1.22bf86p-3f));
+    q = __ffma2_rn(q, f, c2(-0x1.5424e0p-3f));
+    q = __ffma2_rn(q, f, c2(0x1.999fc2p-3f));
+    q = __ffma2_rn(q, f, c2(-0x1.000422p-2f));
+    q = __ffma2_rn(q, f, c2(0x1.555558p-2f));
+    q = __ffma2_rn(q, f, c2(-0x1.fffff8p-2f));
+    const float2 r = __ffma2_rn(__fmul2_rn(f, f), q, f);
+    const float2 Ef = make_float2(__int2float_rn(E0), __int2float_rn(E1));
+    const float2 lnu = __ffma2_rn(Ef, c2(0x1.62e430p-1f), __ffma2_rn(Ef, c2(-0x1.05c610p-29f), r));
+    const float2 v = __ffma2_rn(c2(-2.0f), lnu, c2(0.0f));
+    const float rho0 = __fsqrt_rn(v.x), rho1 = __fsqrt_rn(v.y);
+    // angle: (cos, sin) of pi/2 (q4 + phi)
+    const uint32_t j0 = b0 >> 8, j1 = b1 >> 8;
+    const uint32_t q40 = j0 >> 22, q41 = j1 >> 22;
+    const float2 phi = __fmul2_rn(make_float2(__uint2float_rn(j0 & 0x3FFFFFu), __uint2float_rn(j1 & 0x3FFFFFu)),
+                                  c2(0x1p-22f));
+    const bool s0 = phi.x > 0.5f, s1 = phi.y > 0.5f;
+    const float2 om = __fadd2_rn(c2(1.0f), make_float2(-phi.x, -phi.y));  // fsub_rn(1, phi)
+    const float2 x = make_float2(s0 ? om.x : phi.x, s1 ? om.y : phi.y);
+    const float2 x2 = __fmul2_rn(x, x);
+    float2 ps = c2(0x1.4bdc50p-13f);
+    ps = __ffma2_rn(ps, x2, c2(-0x1.32caf6p-8f));
+    ps = __ffma2_rn(ps, x2, c2(0x1.466bbcp-4f));
+    ps = __ffma2_rn(ps, x2, c2(-0x1.4abbcep-1f));
+    ps = __ffma2_rn(ps, x2, c2(0x1.921fb6p+0f));
+    const float2 sn2 = __fmul2_rn(x, ps);
+    float2 pc = c2(0x1.d9f0a8p-11f);
+    pc = __ffma2_rn(pc, x2, c2(-0x1.55c63cp-6f));
+    pc = __ffma2_rn(pc, x2, c2(0x1.03c1dep-2f));
+    pc = __ffma2_rn(pc, x2, c2(-0x1.3bd3ccp+0f));
+    pc = __ffma2_rn(pc, x2, c2(0x1.000000p+0f));
+    auto rot = [](bool swap, uint32_t q4, float s, float c, float& ct, float& st) {
+        if (swap) {
+            const float t = s;
+            s = c;
+            c = t;
+        }
+        const float cs = (q4 & 1u) ? s : c;
+        const float sn = (q4 & 1u) ? c : s;
+        ct = (q4 == 1u || q4 == 2u) ? -cs : cs;
+        st = (q4 >= 2u) ? -sn : sn;
+    };
+    float ct0, st0, ct1, st1;
+    rot(s0, q40, sn2.x, pc.x, ct0, st0);
+    rot(s1, q41, sn2.y, pc.y, ct1, st1);
+    w0 = __fmul2_rn(__fmul2_rn(make_float2(rho0, rho0), make_float2(ct0, st0)), c2(sc));
+    w1 = __fmul2_rn(__fmul2_rn(make_float2(rho1, rho1), make_float2(ct1, st1)), c2(sc));
+}
+
 }  // namespace tt

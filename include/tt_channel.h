@@ -166,7 +166,9 @@ tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t 
  * chunk sums in chunk order. agg: device float [C / G][n_samples][2]. out: device
  * float [C][n_samples][2] for the per-channel outputs, or NULL (not stored). The input
  * map (tt_channel_set_input_map) applies. May allocate device scratch for the chunk
- * sums on first use or growth (like tt_channel_apply_host's staging).
+ * sums on first use or growth (like tt_channel_apply_host's staging); to capture it in
+ * a CUDA graph, make one call of the same shape before the capture so no allocation
+ * happens inside it.
  * Errors: as tt_channel_apply, plus INVALID_ARG (agg NULL, G <= 0, C % G != 0),
  * OUT_OF_MEMORY. */
 tt_status tt_channel_apply_aggregate(tt_channel_t h, const float* in, float* out, float* agg, int32_t group_size,

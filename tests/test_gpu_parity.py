@@ -337,3 +337,48 @@ def test_device_clock_cuda_graph_replay(cuda_device):
         assert ch.t == calls * n and ch.info().device_clock == 0
     finally:
         ch.close()
+
+
+def test_device_clock_graph_aggregate(cuda_device):
+    """apply_aggregate captured in a CUDA graph (one uncaptured call first allocates its
+    scratch): the replays give the same group sums as eager calls."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    n, calls, G = 2_048, 4, 8
+    w = ttsynth.get("c4").scaled(ues=8, dirs=2, n_per_call=n, calls=calls + 1)
+    run = Run(w, seed=78)
+    xs_all = torch.from_numpy(run.x).to(cuda_device)
+    g_dev = torch.from_numpy(run.gains).to(cuda_device)
+
+    def eager():
+        ch = Channel(run.delays, w.S, seed=run.seed, snapshot_capacity=run.K, device=cuda_device)
+        ch.load_snapshots(g_dev, 0)
+        outs = [ch.apply_aggregate(xs_all[:, c * n:(c + 1) * n].contiguous(), G, noise_sigma=run.sigma).cpu()
+                for c in range(calls + 1)]
+        ch.close()
+        return torch.cat(outs, dim=1).numpy()
+
+    ref = eager()
+    ch = Channel(run.delays, w.S, seed=run.seed, snapshot_capacity=run.K, device=cuda_device)
+    try:
+        ch.load_snapshots(g_dev, 0)
+        x0 = xs_all[:, :n].contiguous()
+        agg0 = ch.apply_aggregate(x0, G, noise_sigma=run.sigma)  # uncaptured: allocates the scratch
+        ch.set_device_clock(True)
+        xin = torch.empty_like(x0)
+        agg = torch.empty_like(agg0)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ch.apply_aggregate(xin, G, agg=agg, noise_sigma=run.sigma)
+        got = [agg0.cpu()]
+        for c in range(1, calls + 1):
+            xin.copy_(xs_all[:, c * n:(c + 1) * n])
+            g.replay()
+            got.append(agg.cpu())
+        ch.set_device_clock(False)
+        assert np.array_equal(torch.cat(got, dim=1).numpy(), ref)
+    finally:
+        ch.close()

@@ -229,7 +229,7 @@ tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream);
  *     UNSUPPORTED), so every call stays on the aligned fast path;
  *   - snapshot residency is not checked per call: the caller keeps the ring loaded for
  *     every slot a graph will replay;
- *   - tt_channel_apply_host returns UNSUPPORTED;
+ *   - tt_channel_apply_host and tt_channel_set_top_n return UNSUPPORTED;
  *   - tt_channel_get_info reports device_clock = 1 and a stale t;
  *   - tt_channel_reset also resets the device clock.
  * enable = 0: synchronises `stream` and reads the device clock back into the handle's

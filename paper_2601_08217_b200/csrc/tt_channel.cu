@@ -814,6 +814,7 @@ tt_status tt_channel_apply_host(tt_channel_t h, const float* in, float* out, int
 
 tt_status tt_channel_set_top_n(tt_channel_t h, int32_t top_n) {
     if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    if (h->dclock) return fail(TT_ERR_UNSUPPORTED, "set_top_n in device-clock mode (it may change the plan)");
     if (top_n < 0) return fail(TT_ERR_INVALID_ARG, "top_n must be >= 0");
     DeviceGuard dg(h->dev);
     const int32_t n = (top_n == 0 || top_n >= h->L) ? 0 : top_n;

@@ -24,9 +24,14 @@
 //    gains h = fma(alpha, dg, g) are formed first (FFMA2), then two packed FMAs per
 //    output into split accumulators A += h_re x, B += h_im x; y = (A.re - B.im, A.im + B.re);
 //  * optional AWGN (docs/tt-normal-v1.md) fused in the epilogue, one Philox call per
-//    sample pair shared by neighbouring lanes via a shuffle;
+//    sample pair shared by neighbouring lanes via a shuffle, the Gaussian transform of
+//    two samples packed into FFMA2/FMUL2/FADD2;
 //  * the consumer warps of a channel's last tile write the new delay-line history from
-//    the staged window into the other half of a ping-pong buffer.
+//    the staged window into the other half of a ping-pong buffer;
+//  * a ROBUST variant (chosen per call by the host) handles calls that do not start on
+//    a 32R-aligned sample (a short lead-in tile) and input rows 8 B off a 16-B boundary
+//    (a per-tile window shift), and can run on the device clock (stream position in
+//    device memory, advanced by the last CTA) for CUDA-graph capture.
 //
 // Every output's operation sequence depends only on (channel, global n) — never on
 // the tile, path or launch shape — so results are bit-identical across partitions.

@@ -237,6 +237,11 @@ tt_status tt_channel_reset(tt_channel_t h, tt_stream_t stream);
  * Calling with the current mode is a no-op. Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
 tt_status tt_channel_set_device_clock(tt_channel_t h, int32_t enable, tt_stream_t stream);
 
+/* Block the calling host thread until all work enqueued on `stream` (NULL = the legacy
+ * default stream) has completed, on the handle's device: lets C callers of the
+ * host-buffer path read their output without the CUDA runtime. Errors: INVALID_ARG, CUDA. */
+tt_status tt_channel_synchronize(tt_channel_t h, tt_stream_t stream);
+
 /* Fill *info. Errors: INVALID_ARG. */
 tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info);
 

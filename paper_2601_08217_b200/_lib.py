@@ -37,6 +37,7 @@ EXPORTS = (
     "tt_synth_jakes",
     "tt_channel_reset",
     "tt_channel_set_device_clock",
+    "tt_channel_synchronize",
     "tt_channel_get_info",
     "tt_channel_destroy",
     "tt_last_error",
@@ -102,11 +103,12 @@ def lib() -> ct.CDLL:
             L.tt_synth_jakes.restype = ct.c_int
             L.tt_channel_reset.argtypes = [P, P]
             L.tt_channel_set_device_clock.argtypes = [P, i32, P]
+            L.tt_channel_synchronize.argtypes = [P, P]
             L.tt_channel_get_info.argtypes = [P, ct.POINTER(ChannelInfo)]
             L.tt_channel_destroy.argtypes = [P]
             for f in ("tt_channel_create", "tt_channel_load_snapshots", "tt_channel_apply", "tt_channel_apply_host",
                       "tt_channel_set_top_n",
-    "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset", "tt_channel_set_device_clock",
+    "tt_channel_set_input_map", "tt_channel_apply_aggregate", "tt_channel_reset", "tt_channel_set_device_clock", "tt_channel_synchronize",
                       "tt_channel_get_info", "tt_channel_destroy"):
                 getattr(L, f).restype = ct.c_int
             L.tt_last_error.argtypes = []
@@ -171,6 +173,10 @@ def tt_channel_reset(h: int, stream: int) -> None:
 
 def tt_channel_set_device_clock(h: int, enable: bool, stream: int) -> None:
     check(lib().tt_channel_set_device_clock(h, 1 if enable else 0, stream))
+
+
+def tt_channel_synchronize(h: int, stream: int) -> None:
+    check(lib().tt_channel_synchronize(h, stream))
 
 
 def tt_channel_get_info(h: int) -> ChannelInfo:

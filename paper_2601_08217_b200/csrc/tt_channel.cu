@@ -1020,6 +1020,13 @@ tt_status tt_channel_set_device_clock(tt_channel_t h, int32_t enable, tt_stream_
     return TT_OK;
 }
 
+tt_status tt_channel_synchronize(tt_channel_t h, tt_stream_t stream) {
+    if (!h) return fail(TT_ERR_INVALID_ARG, "NULL handle");
+    DeviceGuard dg(h->dev);
+    TT_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "stream synchronize");
+    return TT_OK;
+}
+
 tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     if (!h || !info) return fail(TT_ERR_INVALID_ARG, "NULL handle or info");
     info->num_ue = h->C;

@@ -46,6 +46,9 @@ namespace tt {
 constexpr int kConsumerWarps = 16;                   // default tile shape: 16 consumer warps
 constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
 constexpr int kMaxStages = 4;
+#ifndef TT_V
+#define TT_V 0  // kernel variant hook for A/B builds (tools/build_variants.sh); 0 = the product
+#endif
 
 // Stream position kept in device memory (tt_channel_set_device_clock): the kernel
 // reads t and the history parity at its start and its last CTA advances them, so a

@@ -84,6 +84,10 @@ PRESETS = {
 for _L in (1, 4, 16, 64, 256):
     # c5: 1024 UEs x 1,048,576 samples, delays in [0,4L], S=128, no noise; rate assumed 122.88 Msps (R16)
     PRESETS[f"c5-L{_L}"] = Workload(f"c5-L{_L}", 1024, 1, 1_048_576, 1, _L, 4 * _L, 128, None, 122.88e6, 4)
+for _L in (8, 12, 23, 32):
+    # extra points of the same sweep that place the HBM / shared-memory knee (SURVEY §8.4
+    # "Crossover (c5)"); not BASELINE configs
+    PRESETS[f"c5-L{_L}"] = Workload(f"c5-L{_L}", 1024, 1, 1_048_576, 1, _L, 4 * _L, 128, None, 122.88e6, 4)
 
 
 def get(name: str) -> Workload:

@@ -552,16 +552,24 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
         if (GEN && aggdst) {
             // running chunk sum in channel order, kept in the destination row itself (each
             // element is read back only by the thread that wrote it): s = y_first, s += y_k
+            if (first) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int32_t o = obase + r * 32;
-                if (o < ti.Tt) {
-                    if (first) {
-                        aggdst[o] = out[r];
-                    } else {
-                        const float2 v = aggdst[o];
-                        aggdst[o] = make_float2(__fadd_rn(v.x, out[r].x), __fadd_rn(v.y, out[r].y));
-                    }
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * 32;
+                    if (o < ti.Tt) aggdst[o] = out[r];
+                }
+            } else {
+                // all R reads first (independent loads in flight), then the sums
+                float2 v[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * 32;
+                    v[r] = o < ti.Tt ? aggdst[o] : make_float2(0.f, 0.f);
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * 32;
+                    if (o < ti.Tt) aggdst[o] = make_float2(__fadd_rn(v[r].x, out[r].x), __fadd_rn(v[r].y, out[r].y));
                 }
             }
         }

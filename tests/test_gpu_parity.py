@@ -317,6 +317,11 @@ def test_device_clock_cuda_graph_replay(cuda_device):
         ys = [torch.zeros_like(x) for x in xs]
         with pytest.raises(TTError, match="UNSUPPORTED"):
             ch.apply(xs[0][:, :100].contiguous(), noise_sigma=run.sigma)  # n % 256 != 0
+        with pytest.raises(TTError, match="UNSUPPORTED"):
+            ch.set_top_n(2)  # could re-plan away from the tiled kernel
+        xh = xs[0].cpu().pin_memory()
+        with pytest.raises(TTError, match="UNSUPPORTED"):
+            ch.apply_host(xh, torch.empty_like(xh).pin_memory(), noise_sigma=run.sigma)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
@@ -335,6 +340,15 @@ def test_device_clock_cuda_graph_replay(cuda_device):
         assert np.array_equal(out, eager)
         ch.set_device_clock(False)
         assert ch.t == calls * n and ch.info().device_clock == 0
+    finally:
+        ch.close()
+    # entering the mode off the 256-sample grid is refused
+    ch = Channel(run.delays, w.S, seed=run.seed, snapshot_capacity=run.K, device=cuda_device)
+    try:
+        ch.load_snapshots(torch.from_numpy(run.gains).to(cuda_device), 0)
+        ch.apply(torch.zeros((run.C, 100, 2), dtype=torch.float32, device=cuda_device), noise_sigma=run.sigma)
+        with pytest.raises(TTError, match="UNSUPPORTED"):
+            ch.set_device_clock(True)
     finally:
         ch.close()
 

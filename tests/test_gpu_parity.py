@@ -259,14 +259,18 @@ def test_random_instances_vs_oracle(cuda_device):
 
     from paper_2601_08217_b200 import Channel
 
-    rng = np.random.default_rng(2026)
+    import os
+
+    # TT_FUZZ_INSTANCES / TT_FUZZ_SEED / TT_FUZZ_MAX_N widen the sweep for stress runs
+    rng = np.random.default_rng(int(os.environ.get("TT_FUZZ_SEED", "2026")))
+    max_n = int(os.environ.get("TT_FUZZ_MAX_N", "4096"))
     kinds = set()
-    for inst in range(60):
+    for inst in range(int(os.environ.get("TT_FUZZ_INSTANCES", "60"))):
         C = int(rng.integers(1, 6))
         L = int(rng.integers(1, 101))
         D = int(rng.integers(L - 1, 4 * L + 50)) if L > 1 else int(rng.integers(0, 50))
         S = int(rng.choice([1, 3, 16, 32, 64, 100, 128, 256, 333, 512, 1024]))
-        N = int(rng.integers(1, 4097))
+        N = int(rng.integers(1, max_n + 1))
         sigma = float(rng.choice([0.0, 0.05]))
         d = np.stack([np.sort(rng.choice(D + 1, L, replace=D + 1 < L)) for _ in range(C)]).astype(np.int32)
         K = (N - 1) // S + 2

@@ -276,3 +276,60 @@ def test_synthesised_channel_end_to_end(cuda_device):
         y = ch.apply(torch.from_numpy(x).to(cuda_device)).cpu().numpy()
     ref = oracle.convolve(dr, S, gr, 0, x, 0, 0, N)
     compare(y, ref, "synthesised channel")
+
+
+def test_random_next_instances(cuda_device):
+    """Property sweep over the NEXT rows: random shapes, snapshot periods, noise and
+    call splits for f1 group sums (random G dividing C) and f2 top-n taps; each against
+    the oracle, streamed == one-shot bit for bit. TT_FUZZ_INSTANCES / TT_FUZZ_SEED widen
+    it for stress runs."""
+    import os
+
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    rng = np.random.default_rng(int(os.environ.get("TT_FUZZ_SEED", "2027")))
+    for inst in range(int(os.environ.get("TT_FUZZ_INSTANCES", "20"))):
+        G = int(rng.integers(1, 20))
+        C = G * int(rng.integers(1, 4))
+        L = int(rng.integers(2, 60))
+        D = int(rng.integers(L - 1, 4 * L + 50))
+        S = int(rng.choice([16, 64, 100, 128, 256, 512]))
+        N = int(rng.integers(1, 12_001))
+        sigma = float(rng.choice([0.0, 0.05]))
+        top_n = int(rng.integers(1, L))
+        d = np.stack([np.sort(rng.choice(D + 1, L, replace=False)) for _ in range(C)]).astype(np.int32)
+        K = (N - 1) // S + 2
+        g = (rng.standard_normal((C, K, L, 2)) / np.sqrt(2 * L)).astype(np.float32)
+        x = (rng.standard_normal((C, N, 2)) * np.sqrt(0.5)).astype(np.float32)
+        cut = int(rng.integers(1, N)) if N > 1 else N
+        splits = ([cut, N - cut] if N > 1 else [N], [N])
+        gd = torch.from_numpy(g).to(cuda_device)
+        aggs, ys_sparse = [], []
+        for split in splits:
+            ch = Channel(d, S, seed=inst, snapshot_capacity=K, device=cuda_device)
+            ch.load_snapshots(gd, 0)
+            a, pos = [], 0
+            for n in split:
+                a.append(ch.apply_aggregate(torch.from_numpy(np.ascontiguousarray(x[:, pos:pos + n])).to(cuda_device),
+                                            G, noise_sigma=sigma).cpu().numpy())
+                pos += n
+            ch.close()
+            aggs.append(np.concatenate(a, axis=1))
+            ch = Channel(d, S, seed=inst, snapshot_capacity=K, device=cuda_device)
+            ch.set_top_n(top_n)
+            ch.load_snapshots(gd, 0)
+            yv, pos = [], 0
+            for n in split:
+                yv.append(ch.apply(torch.from_numpy(np.ascontiguousarray(x[:, pos:pos + n])).to(cuda_device),
+                                   noise_sigma=sigma).cpu().numpy())
+                pos += n
+            ch.close()
+            ys_sparse.append(np.concatenate(yv, axis=1))
+        what = f"instance {inst}: G={G} C={C} L={L} D={D} S={S} N={N} top_n={top_n}"
+        assert np.array_equal(aggs[0], aggs[1]) and np.array_equal(ys_sparse[0], ys_sparse[1]), what
+        ref = oracle.convolve(d, S, g, 0, x, 0, 0, N, sigma=sigma, seed=inst)
+        compare(aggs[0], oracle.aggregate(ref, G), "agg " + what)
+        ref_s = oracle.convolve(d, S, g, 0, x, 0, 0, N, sigma=sigma, seed=inst, top_n=top_n)
+        compare(ys_sparse[0], ref_s, "sparse " + what)

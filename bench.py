@@ -149,6 +149,17 @@ def _traffic(config: str):
         return None
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(w: ttsynth.Workload, target_s: float = 10.0):
     """The oracle (as it stands) on this host's cores, on a bounded sample of the
     workload: whole slots of the first channels, grown until ~target_s of wall time."""
@@ -179,7 +190,7 @@ def cpu_baseline(w: ttsynth.Workload, target_s: float = 10.0):
     oracle.convolve(d, w.S, g, 0, x, 0, 0, N, sigma=w.sigma, seed=0)
     elapsed = time.perf_counter() - t0
     done = c * N
-    return {"value": done / elapsed, "unit": "samples/s", "cores": cores, "kind": "oracle",
+    return {"value": done / elapsed, "unit": "samples/s", "cores": cores, "kind": "oracle", "cpu": _cpu_model(),
             "sample": f"{c} of {w.C} channels x {slots} consecutive slots of {n} samples of {w.name} "
                       f"({done} samples, {elapsed:.2f} s wall, double precision, OpenMP over {cores} threads)"}
 
@@ -222,7 +233,7 @@ def run_reference(args, w):
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(w, world),
-        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": cores, "kind": "oracle", "cpu": _cpu_model(),
                          "sample": f"{c} of {w.C} channels x 1 slot of {n} samples per step"},
         "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "realtime_ues": w.realtime_ues(val),

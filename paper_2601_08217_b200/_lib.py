@@ -139,7 +139,10 @@ def tt_channel_load_snapshots(h: int, gains_ptr: int, first_index: int, count: i
 
 
 def tt_channel_apply(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_sigma: float, stream: int) -> None:
-    check(lib().tt_channel_apply(h, in_ptr, out_ptr, n_samples, noise_sigma, stream))
+    L = _lib if _lib is not None else lib()  # hot path: skip the loader lock once loaded
+    st = L.tt_channel_apply(h, in_ptr, out_ptr, n_samples, noise_sigma, stream)
+    if st != TT_OK:
+        check(st)
 
 
 def tt_channel_apply_host(h: int, in_ptr: int, out_ptr: int, n_samples: int, noise_sigma: float,

@@ -88,21 +88,30 @@ class Channel:
     def apply(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, noise_sigma: float = 0.0,
               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
         """x: float32 device tensor [C][n][2] (or complex64 [C][n]); returns y alike."""
-        xv = torch.view_as_real(x) if x.is_complex() else x
+        cplx = x.is_complex()
+        xv = torch.view_as_real(x) if cplx else x
         rows = getattr(self, "in_rows", self.C)
-        if xv.dtype != torch.float32 or xv.dim() != 3 or xv.shape[0] != rows or xv.shape[2] != 2:
+        shape = xv.shape
+        if xv.dtype != torch.float32 or len(shape) != 3 or shape[0] != rows or shape[2] != 2:
             raise ValueError(f"x must be float32 [{rows}][n][2] or complex64 [{rows}][n]")
         if not xv.is_contiguous():
             raise ValueError("x must be contiguous")
+        n = shape[1]
         if out is None:
-            out = torch.empty((self.C,) + tuple(xv.shape[1:]), dtype=torch.float32, device=xv.device)
-            if x.is_complex():
+            out = torch.empty((self.C, n, 2), dtype=torch.float32, device=xv.device)
+            if cplx:
                 out = torch.view_as_complex(out)
-        ov = torch.view_as_real(out) if out.is_complex() else out
-        if ov.shape != (self.C,) + tuple(xv.shape[1:]) or not ov.is_contiguous() or ov.dtype != torch.float32:
-            raise ValueError(f"out must be contiguous float32 [C={self.C}][n][2]")
-        _lib.tt_channel_apply(self.handle, xv.data_ptr(), ov.data_ptr(), int(xv.shape[1]), float(noise_sigma),
-                              _stream_ptr(stream))
+            ov = torch.view_as_real(out) if cplx else out
+        else:
+            ov = torch.view_as_real(out) if out.is_complex() else out
+            oshape = ov.shape
+            if len(oshape) != 3 or oshape[0] != self.C or oshape[1] != n or oshape[2] != 2 or \
+                    not ov.is_contiguous() or ov.dtype != torch.float32:
+                raise ValueError(f"out must be contiguous float32 [C={self.C}][n][2]")
+        h = self._h
+        if h is None:
+            raise RuntimeError("channel is closed")
+        _lib.tt_channel_apply(h, xv.data_ptr(), ov.data_ptr(), n, float(noise_sigma), _stream_ptr(stream))
         return out
 
     def set_top_n(self, top_n: int) -> None:

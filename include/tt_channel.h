@@ -117,7 +117,11 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
  * library detects which); the copy is enqueued on `stream` and the source must stay
  * valid until it completes there. If the new block is contiguous with the resident
  * range the range grows (older snapshots fall out once capacity is exceeded);
- * otherwise the resident range is replaced by the new block.
+ * otherwise the resident range is replaced by the new block. A block that starts
+ * inside the resident range may also end inside it (a reload of snapshots already
+ * resident): the snapshots after it stay resident and the interpolation across the
+ * block's both ends uses the new values (the differences to the resident neighbours
+ * first-1 and first+count are recomputed).
  * Errors: INVALID_ARG (NULL handle/gains, first_index < 0, count <= 0,
  *   count > capacity), CUDA. */
 tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t first_index, int64_t count,

@@ -13,9 +13,18 @@ import torch
 from . import _lib
 
 
-def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_ptr(stream: Optional[torch.cuda.Stream], device: Optional[torch.device] = None) -> int:
+    """The given stream, else the current stream of `device` (the channel's device,
+    not whatever device happens to be current)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
+
+
+def _check_dev(name: str, t: torch.Tensor, device: torch.device) -> None:
+    # a CPU tensor or one on another GPU would reach the kernel as a foreign pointer
+    # and fault the context: refuse it here
+    if t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
 
 
 class Channel:
@@ -28,7 +37,11 @@ class Channel:
             raise ValueError("delays must be [C][L]")
         self.C, self.L = int(d.shape[0]), int(d.shape[1])
         self.S = int(snapshot_period)
-        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        if dev.type != "cuda":
+            raise ValueError(f"a Channel lives on a CUDA device, got {dev}")
+        # an explicit index, so tensor-device checks compare like with like
+        self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
         self._h = None
         with torch.cuda.device(self.device):
             self._h = _lib.tt_channel_create(self.C, self.L, d.ctypes.data, self.S, int(seed), int(snapshot_capacity),
@@ -80,7 +93,9 @@ class Channel:
             keep = g
         if tuple(keep.shape[:1]) != (self.C,) or keep.shape[2:] != (self.L, 2):
             raise ValueError(f"gains must be [C={self.C}][count][L={self.L}][2], got {tuple(keep.shape)}")
-        _lib.tt_channel_load_snapshots(self.handle, ptr, int(first_index), int(count), _stream_ptr(stream))
+        if not isinstance(keep, np.ndarray) and keep.device.type == "cuda":
+            _check_dev("gains", keep, self.device)
+        _lib.tt_channel_load_snapshots(self.handle, ptr, int(first_index), int(count), _stream_ptr(stream, self.device))
         if isinstance(keep, np.ndarray):
             # host pageable source: make sure the copy has consumed it before returning
             torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
@@ -96,6 +111,8 @@ class Channel:
             raise ValueError(f"x must be float32 [{rows}][n][2] or complex64 [{rows}][n]")
         if not xv.is_contiguous():
             raise ValueError("x must be contiguous")
+        dev = self.device
+        _check_dev("x", xv, dev)
         n = shape[1]
         if out is None:
             out = torch.empty((self.C, n, 2), dtype=torch.float32, device=xv.device)
@@ -108,10 +125,11 @@ class Channel:
             if len(oshape) != 3 or oshape[0] != self.C or oshape[1] != n or oshape[2] != 2 or \
                     not ov.is_contiguous() or ov.dtype != torch.float32:
                 raise ValueError(f"out must be contiguous float32 [C={self.C}][n][2]")
+            _check_dev("out", ov, dev)
         h = self._h
         if h is None:
             raise RuntimeError("channel is closed")
-        _lib.tt_channel_apply(h, xv.data_ptr(), ov.data_ptr(), n, float(noise_sigma), _stream_ptr(stream))
+        _lib.tt_channel_apply(h, xv.data_ptr(), ov.data_ptr(), n, float(noise_sigma), _stream_ptr(stream, dev))
         return out
 
     def set_top_n(self, top_n: int) -> None:
@@ -143,20 +161,23 @@ class Channel:
         if xv.dtype != torch.float32 or xv.dim() != 3 or xv.shape[0] != rows or xv.shape[2] != 2 or \
                 not xv.is_contiguous():
             raise ValueError(f"x must be contiguous float32 [{rows}][n][2]")
+        _check_dev("x", xv, self.device)
         n = int(xv.shape[1])
         if group_size <= 0 or self.C % group_size:
             raise ValueError(f"group_size must divide C={self.C}")
         if agg is None:
             agg = torch.empty((self.C // group_size, n, 2), dtype=torch.float32, device=xv.device)
-        if agg.shape != (self.C // group_size, n, 2) or not agg.is_contiguous():
+        if agg.shape != (self.C // group_size, n, 2) or not agg.is_contiguous() or agg.dtype != torch.float32:
             raise ValueError("agg must be contiguous float32 [C/group_size][n][2]")
+        _check_dev("agg", agg, self.device)
         optr = 0
         if out is not None:
             if out.shape != (self.C, n, 2) or not out.is_contiguous() or out.dtype != torch.float32:
                 raise ValueError("out must be contiguous float32 [C][n][2]")
+            _check_dev("out", out, self.device)
             optr = out.data_ptr()
         _lib.tt_channel_apply_aggregate(self.handle, xv.data_ptr(), optr, agg.data_ptr(), int(group_size), n,
-                                        float(noise_sigma), _stream_ptr(stream))
+                                        float(noise_sigma), _stream_ptr(stream, self.device))
         return agg
 
     def apply_host(self, x: torch.Tensor, out: torch.Tensor, noise_sigma: float = 0.0,
@@ -168,17 +189,17 @@ class Channel:
                 out.shape != x.shape or not (x.is_contiguous() and out.is_contiguous()):
             raise ValueError(f"x, out must be contiguous float32 [C={self.C}][n][2]")
         _lib.tt_channel_apply_host(self.handle, x.data_ptr(), out.data_ptr(), int(x.shape[1]), float(noise_sigma),
-                                   _stream_ptr(stream))
+                                   _stream_ptr(stream, self.device))
         return out
 
     def reset(self, stream: Optional[torch.cuda.Stream] = None) -> None:
-        _lib.tt_channel_reset(self.handle, _stream_ptr(stream))
+        _lib.tt_channel_reset(self.handle, _stream_ptr(stream, self.device))
 
     def set_device_clock(self, enable: bool, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Device-clock mode (tt_channel_set_device_clock): the stream position lives on
         the GPU, so slot calls can be captured into a CUDA graph and replayed; calls
         then need n % 256 == 0 and snapshot residency is the caller's contract."""
-        _lib.tt_channel_set_device_clock(self.handle, enable, _stream_ptr(stream))
+        _lib.tt_channel_set_device_clock(self.handle, enable, _stream_ptr(stream, self.device))
 
 
 def synth_jakes(path_delay, path_power, num_sinusoids: int, nu: float, seed: int, first_index: int, count: int,
@@ -198,5 +219,5 @@ def synth_jakes(path_delay, path_power, num_sinusoids: int, nu: float, seed: int
     with torch.cuda.device(dev):
         _lib.tt_synth_jakes(t.ctypes.data, w.ctypes.data, C, P, int(num_sinusoids), float(nu), int(seed),
                             int(channel_offset), int(first_index), int(count), d.ctypes.data, g.data_ptr(),
-                            _stream_ptr(stream))
+                            _stream_ptr(stream, dev))
     return d, g

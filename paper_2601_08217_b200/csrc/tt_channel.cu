@@ -139,9 +139,12 @@ struct tt_channel_s {
 
 namespace {
 
+// The attribute is per kernel function for the whole process, not per handle: it is
+// set to the shape's full budget (never to one handle's size), so creating a handle
+// with a smaller plan can never lower the cap of handles already alive.
 template <int R, int CW, bool NOISE>
-cudaError_t prepare_kernel(size_t smem) {
-    const int sm = static_cast<int>(smem);
+cudaError_t prepare_kernel(size_t budget) {
+    const int sm = static_cast<int>(budget);
     for (cudaError_t e : {cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false, false>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                           cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, false>,
@@ -191,12 +194,13 @@ cudaError_t prepare_tiled(tt_channel_s* h) {
         tp.nk_max = nk;
         break;
     }
+    const size_t budget = tp.ctas == 1 ? kSmemBudget : 112 * 1024;
     switch (tp.R * 100 + tp.CW) {
-        case 816: return prepare_kernel<8, 16, NOISE>(tp.smem);
-        case 1608: return prepare_kernel<16, 8, NOISE>(tp.smem);
-        case 808: return prepare_kernel<8, 8, NOISE>(tp.smem);
-        case 416: return prepare_kernel<4, 16, NOISE>(tp.smem);
-        case 216: return prepare_kernel<2, 16, NOISE>(tp.smem);
+        case 816: return prepare_kernel<8, 16, NOISE>(budget);
+        case 1608: return prepare_kernel<16, 8, NOISE>(budget);
+        case 808: return prepare_kernel<8, 8, NOISE>(budget);
+        case 416: return prepare_kernel<4, 16, NOISE>(budget);
+        case 216: return prepare_kernel<2, 16, NOISE>(budget);
         default: return cudaSuccess;  // generic kernel
     }
 }
@@ -240,11 +244,12 @@ cudaError_t prepare_rw(tt_channel_s* h) {
     }
     cudaError_t e;
     if ((e = cudaMemcpy(h->tab, tb.data(), tb.size() * sizeof(int2), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    // process-wide attribute: the full budget, not this handle's size (see prepare_kernel)
     if ((e = cudaFuncSetAttribute(NS::template kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sm))) != cudaSuccess)
+                                  static_cast<int>(kSmemBudget))) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(NS::template kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sm))) != cudaSuccess)
+                                  static_cast<int>(kSmemBudget))) != cudaSuccess)
         return e;
     h->plan.rw_R = R;
     h->plan.rw_wbytes = static_cast<int>(wbytes);
@@ -699,9 +704,17 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
                           count <= h->cap - 1)
                              ? 1
                              : 0;
+    // a block reloaded inside the resident range (it ends before res_hi): snapshot
+    // first + count stays resident, so the block's last difference is completed against
+    // it now (else that row would keep dg = 0 while intervals through it stay accepted)
+    const int64_t hi_new = first_index + count;
+    const int fix_next = (h->res_hi > h->res_lo && first_index >= h->res_lo && first_index <= h->res_hi &&
+                          hi_new < h->res_hi && count <= h->cap - 1)
+                             ? 1
+                             : 0;
     const int64_t grid = std::min<int64_t>((static_cast<int64_t>(elems) + 255) / 256, int64_t(h->num_sms) * 16);
     tt::tt_load_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), 256, 0, st>>>(
-        src, count, first_index, h->ring, h->cap, h->perm, h->C, h->L, fix_prev);
+        src, count, first_index, h->ring, h->cap, h->perm, h->C, h->L, fix_prev, fix_next);
     TT_CUDA(cudaGetLastError(), "snapshot loader launch");
     {
         // sparse rows follow the dense rows they are selected from (the previous row's
@@ -820,28 +833,45 @@ tt_status tt_channel_set_top_n(tt_channel_t h, int32_t top_n) {
     const int32_t n = (top_n == 0 || top_n >= h->L) ? 0 : top_n;
     if (n == h->top_n) return TT_OK;
     TT_CUDA(cudaDeviceSynchronize(), "top-n drain");
-    cudaFree(h->sring);
-    cudaFree(h->soff);
-    h->sring = nullptr;
-    h->soff = nullptr;
-    h->top_n = 0;
-    h->n4 = 0;
+    // back to the dense state first; any failure below leaves the handle dense with a
+    // dense plan (the plan always matches top_n: a sparse plan stages L = top_n wide
+    // coefficient rows and would overrun shared memory on a dense apply)
+    auto to_dense = [h]() {
+        cudaFree(h->sring);
+        cudaFree(h->soff);
+        h->sring = nullptr;
+        h->soff = nullptr;
+        h->top_n = 0;
+        h->n4 = 0;
+    };
+    auto fail_dense = [h, &to_dense](cudaError_t e, const char* what) {
+        to_dense();
+        const tt_status s = cuda_fail(e, what);
+        const cudaError_t pe = prepare_plan(h);
+        if (pe != cudaSuccess) cudaGetLastError();
+        return s;
+    };
+    to_dense();
+    cudaError_t e = cudaSuccess;
     if (n > 0) {
         const int32_t n4 = (n + 1 + 3) & ~3;
-        TT_CUDA(cudaMalloc(&h->sring, (static_cast<size_t>(h->C) * h->cap * n + 1) * sizeof(float4)),
-                "cudaMalloc(sparse ring)");
-        TT_CUDA(cudaMalloc(&h->soff, static_cast<size_t>(h->C) * h->cap * n4 * sizeof(int32_t)),
-                "cudaMalloc(sparse offsets)");
-        TT_CUDA(cudaMemset(h->sring, 0, (static_cast<size_t>(h->C) * h->cap * n + 1) * sizeof(float4)), "zero ring");
-        TT_CUDA(cudaMemset(h->soff, 0, static_cast<size_t>(h->C) * h->cap * n4 * sizeof(int32_t)), "zero offsets");
+        const size_t ring_b = (static_cast<size_t>(h->C) * h->cap * n + 1) * sizeof(float4);
+        const size_t off_b = static_cast<size_t>(h->C) * h->cap * n4 * sizeof(int32_t);
+        if ((e = cudaMalloc(&h->sring, ring_b)) != cudaSuccess) return fail_dense(e, "cudaMalloc(sparse ring)");
+        if ((e = cudaMalloc(&h->soff, off_b)) != cudaSuccess) return fail_dense(e, "cudaMalloc(sparse offsets)");
+        if ((e = cudaMemset(h->sring, 0, ring_b)) != cudaSuccess) return fail_dense(e, "zero ring");
+        if ((e = cudaMemset(h->soff, 0, off_b)) != cudaSuccess) return fail_dense(e, "zero offsets");
+        // process-wide attribute: the largest any handle can need (4 warps x TT_MAX_TAPS
+        // magnitudes), so a later handle with fewer taps never lowers it
+        if (h->L * sizeof(float) * 4 > 48 * 1024 &&
+            (e = cudaFuncSetAttribute(tt::tt_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(TT_MAX_TAPS * sizeof(float) * 4))) != cudaSuccess)
+            return fail_dense(e, "selection smem");
         h->top_n = n;
         h->n4 = n4;
-        if (h->L * sizeof(float) * 4 > 48 * 1024)
-            TT_CUDA(cudaFuncSetAttribute(tt::tt_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(h->L * sizeof(float) * 4)),
-                    "selection smem");
     }
-    cudaError_t e = prepare_plan(h);
+    e = prepare_plan(h);
+    if (e != cudaSuccess && h->top_n > 0) return fail_dense(e, "plan");
     if (e != cudaSuccess) return cuda_fail(e, "plan");
     if (h->top_n > 0 && h->res_hi > h->res_lo) {
         tt_status s = select_rows(h, h->res_lo, h->res_hi - h->res_lo, nullptr);
@@ -857,9 +887,7 @@ tt_status tt_channel_set_input_map(tt_channel_t h, const int32_t* rows, int32_t 
     if (!rows) {
         if (h->in_row) {
             TT_CUDA(cudaDeviceSynchronize(), "input map drain");
-            cudaFree(h->in_row);
-    cudaFree(h->sring);
-    cudaFree(h->soff);
+            cudaFree(h->in_row);  // the map owns only its row table, never the sparse ring
         }
         h->in_row = nullptr;
         h->in_rows = 0;

@@ -879,9 +879,13 @@ __global__ void tt_select_kernel(const float4* __restrict__ ring, float4* __rest
 // count - 1 of every channel into the ring as (g_k, g_{k+1} - g_k) in sorted-tap order.
 // src: device float2 [C][count][L] in the caller's (original) tap order; perm [C][L]:
 // original index of sorted tap j. The difference of the last new snapshot is completed
-// by the next contiguous load; `fix_prev` completes snapshot first - 1's difference.
+// by the next contiguous load; `fix_prev` completes snapshot first - 1's difference;
+// `fix_next` (a block reloaded inside the resident range, so snapshot first + count
+// stays resident) completes the last new snapshot's difference against the ring's copy
+// of snapshot first + count.
 __global__ void tt_load_kernel(const float2* __restrict__ src, int64_t count, int64_t first, float4* ring, int64_t cap,
-                               const int32_t* __restrict__ perm, int32_t C, int32_t L, int32_t fix_prev) {
+                               const int32_t* __restrict__ perm, int32_t C, int32_t L, int32_t fix_prev,
+                               int32_t fix_next) {
     const int64_t tot = static_cast<int64_t>(C) * count * L;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -892,12 +896,17 @@ __global__ void tt_load_kernel(const float2* __restrict__ src, int64_t count, in
         const int32_t o = __ldg(perm + c * L + j);
         const float2 g = __ldg(src + (c * count + i) * L + o);
         float4 v = make_float4(g.x, g.y, 0.f, 0.f);
+        const int64_t k = first + i;
         if (i + 1 < count) {
             const float2 g1 = __ldg(src + (c * count + i + 1) * L + o);
             v.z = __fsub_rn(g1.x, g.x);
             v.w = __fsub_rn(g1.y, g.y);
+        } else if (fix_next) {
+            // snapshot k + 1 is resident and not rewritten by this load (count < cap)
+            const float4 nx = ring[(c * cap + (k + 1) % cap) * L + j];
+            v.z = __fsub_rn(nx.x, g.x);
+            v.w = __fsub_rn(nx.y, g.y);
         }
-        const int64_t k = first + i;
         ring[(c * cap + k % cap) * L + j] = v;
         if (i == 0 && fix_prev) {
             float4* pv = ring + (c * cap + (k - 1) % cap) * L + j;

@@ -85,11 +85,15 @@ typedef struct {
 } tt_channel_info;
 
 /* kernels a plan can select (all compute the same per-output operation sequence, so
- * their outputs are bit-identical; the environment variable TT_KERNEL=rw|tiled|generic
+ * their outputs are bit-identical; the environment variable TT_KERNEL=dw|rw|tiled|generic
  * read at create restricts the choice) */
 #define TT_KERNEL_GENERIC 0 /* one thread per output, operands from global memory */
 #define TT_KERNEL_TILED 1   /* TMA-staged tiles, lane-strided outputs, x from shared memory */
 #define TT_KERNEL_RW 2      /* register-window kernel: 16 consecutive outputs per thread */
+#define TT_KERNEL_DW 3      /* dense-window kernel (opt-in, TT_KERNEL=dw): 16 consecutive outputs
+                               per thread from two 16-sample x blocks in registers, window and
+                               outputs moved by 2-D TMA tensor copies (128-B swizzle); calls whose
+                               start or length is not a multiple of 16 run the tiled kernel */
 
 /* Create a handle for C = num_ue channels with L = num_taps taps each.
  *   delays: host int32 [C][L], each in [0, TT_MAX_DELAY]; duplicates allowed (the

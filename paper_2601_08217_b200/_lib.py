@@ -75,7 +75,7 @@ class ChannelInfo(ct.Structure):
     ]
 
 
-KERNELS = {0: "generic", 1: "tiled", 2: "rw"}
+KERNELS = {0: "generic", 1: "tiled", 2: "rw", 3: "dw"}
 
 
 _lock = threading.Lock()

@@ -18,7 +18,7 @@ SO = os.path.join(PKG, "libtt.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["tt_channel.cu"]
-HEADERS = ["tt_conv.cuh", "tt_conv_rw.cuh", "tt_conv_rw_body.inc", "tt_noise.cuh", "tt_synth.cuh"]
+HEADERS = ["tt_conv.cuh", "tt_conv_dw.cuh", "tt_conv_rw.cuh", "tt_conv_rw_body.inc", "tt_noise.cuh", "tt_synth.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

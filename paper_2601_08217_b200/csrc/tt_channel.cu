@@ -17,6 +17,7 @@
 
 #include "tt_channel.h"
 #include "tt_conv.cuh"
+#include "tt_conv_dw.cuh"
 #include "tt_conv_rw.cuh"
 #include "tt_synth.cuh"
 
@@ -65,8 +66,19 @@ struct TiledPlan {
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;      // gain rows staged per tile
 };
+// dense-window kernel (tt_conv_dw.cuh): chosen for taps dense in delay
+struct DwPlan {
+    int CW = 0;            // consumer warps (0: not planned)
+    int stages = 0;
+    int nk_max = 0;        // gain rows staged per tile
+    int win_rows = 0;      // window rows per stage
+    int stage_bytes = 0;   // multiple of 1024
+    int coef_off = 0, tab_off = 0;
+    size_t smem = 0;       // dynamic shared memory (incl. alignment slack)
+};
 struct Plan {
     int kind = TT_KERNEL_GENERIC;
+    DwPlan dw;
     TiledPlan tiled[2];  // [noise]
     // register-window kernel (opt-in: TT_KERNEL=rw)
     int rw_R = 0, rw_wbytes = 0, rw_rows = 0, rw_row_stride = 0, rw_sbytes = 0;
@@ -111,6 +123,8 @@ struct tt_channel_s {
     int32_t* perm = nullptr;   // [C][L] original tap index of sorted tap j
     int32_t* xoff = nullptr;   // [C][L4] window offset H - d_j of sorted tap j
     int2* tab = nullptr;       // [C][L + 1] register-window table: (window byte offset, fresh samples)
+    int32_t* dwtab = nullptr;  // [C][L4] dense-window tap table: f | dq class << 4 | q << 8 (d = 16 q + f)
+    CUtensorMap dw_hist[3];    // history tensor maps: [0], [1] ping-pong halves, [2] the zero buffer
     std::vector<int32_t> sorted_d;  // [C][L] delays in sorted-tap order (host; rebuilds the rw table)
     int32_t* in_row = nullptr;  // [C] input row per channel (NEXT f4), nullptr = identity
     tt::DevClock* dclk = nullptr;  // device clock (stream position for graph-captured slot loops)
@@ -302,6 +316,108 @@ void launch_rw(tt_channel_s* h, const tt::ConvParams& p, const float2* x, float2
         NS::template kernel<false>()<<<static_cast<unsigned>(grid), NS::kThreads, h->plan.rw_smem, st>>>(q);
 }
 
+// ---- 2-D/3-D TMA tensor maps (dense-window kernel) ---------------------------------
+// cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point query,
+// so libtt.so has no link-time dependency on libcuda (it loads on hosts without a GPU).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+
+// A [planes][rows][16 complex samples] view of float2 rows (one row = 128 B), boxes of
+// box_rows rows of one plane, 128-B swizzle in shared memory, zero fill out of bounds.
+bool encode_rows(CUtensorMap* m, const void* base, uint64_t rows, uint64_t planes, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || rows == 0 || planes == 0) return false;
+    const cuuint64_t dims[3] = {32, rows, planes};
+    const cuuint64_t strides[2] = {128, rows * 128};
+    const cuuint32_t box[3] = {32, box_rows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CW, bool NOISE>
+cudaError_t prepare_dw_kernel() {
+    return cudaFuncSetAttribute(tt::dw::tt_conv_dw_kernel<CW, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemBudget));  // process-wide: the full budget
+}
+
+// Dense-window plan (tt_conv_dw.cuh; opt-in with TT_KERNEL=dw). A thread reads about
+// (D + 32) / (16 L) x samples per output-tap from shared memory instead of 1.
+cudaError_t prepare_dw(tt_channel_s* h) {
+    DwPlan& dp = h->plan.dw;
+    dp = DwPlan{};
+    if (h->top_n > 0 || h->S % 16 != 0 || h->H % 16 != 0) return cudaSuccess;
+    if (!encode_fn()) return cudaSuccess;
+    const int Hw = (h->H + 127) & ~127;
+    // consumer warps: 7 (+ the producer = 8 warps, 2 per SMSP: up to 255 registers per
+    // thread, no spills; 8 + 1 warps cap the kernel at 168 and spill); TT_DW_WARPS=8|4 for
+    // experiments; 4 when the stage does not fit
+    int first_cw = 7;
+    if (const char* fw = getenv("TT_DW_WARPS"))
+        if (*fw) first_cw = atoi(fw);
+    for (int CW : {first_cw, 4}) {
+        if (CW != 8 && CW != 7 && CW != 4) continue;
+        const int T = CW * 32 * tt::dw::R;
+        if (Hw > T) continue;
+        const int nk = (T - 1) / h->S + 2;
+        const int win_rows = (((Hw + T) / 16) + tt::dw::kXBoxRows - 1) / tt::dw::kXBoxRows * tt::dw::kXBoxRows;
+        const size_t win_b = static_cast<size_t>(win_rows) * tt::dw::kRowBytes;
+        const size_t coef_b = (static_cast<size_t>(nk) * h->L * 16 + 16 + 15) & ~size_t(15);
+        const size_t tab_b = static_cast<size_t>(h->L4) * 4;
+        const size_t stage = (win_b + coef_b + tab_b + 1023) & ~size_t(1023);
+        const size_t fixed = 1024 + 1024 + static_cast<size_t>(CW) * 32 * tt::dw::kRowBytes;
+        int stages = tt::dw::kMaxStages;
+        while (stages >= 2 && fixed + stages * stage > kSmemBudget) --stages;
+        if (stages < 2) continue;
+        if (stage > (size_t(1) << 30)) continue;
+        dp.CW = CW;
+        dp.stages = stages;
+        dp.nk_max = nk;
+        dp.win_rows = win_rows;
+        dp.stage_bytes = static_cast<int>(stage);
+        dp.coef_off = static_cast<int>(win_b);
+        dp.tab_off = static_cast<int>(win_b + coef_b);
+        dp.smem = fixed + stages * stage;
+        break;
+    }
+    if (!dp.CW) return cudaSuccess;
+    const size_t hs = static_cast<size_t>(h->C) * h->H;
+    if (!encode_rows(&h->dw_hist[0], h->hist, h->H / 16, h->C, tt::dw::kHBoxRows) ||
+        !encode_rows(&h->dw_hist[1], h->hist + hs, h->H / 16, h->C, tt::dw::kHBoxRows) ||
+        !encode_rows(&h->dw_hist[2], h->hist_zero, h->H / 16, h->C, tt::dw::kHBoxRows)) {
+        dp = DwPlan{};
+        return cudaSuccess;
+    }
+    cudaError_t e;
+    if (dp.CW == 8) {
+        if ((e = prepare_dw_kernel<8, false>()) != cudaSuccess || (e = prepare_dw_kernel<8, true>()) != cudaSuccess)
+            return e;
+    } else if (dp.CW == 7) {
+        if ((e = prepare_dw_kernel<7, false>()) != cudaSuccess || (e = prepare_dw_kernel<7, true>()) != cudaSuccess)
+            return e;
+    } else {
+        if ((e = prepare_dw_kernel<4, false>()) != cudaSuccess || (e = prepare_dw_kernel<4, true>()) != cudaSuccess)
+            return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t prepare_plan(tt_channel_s* h) {
     h->plan = Plan{};
     // TT_KERNEL=rw|tiled|generic selects the kernel (all are bit-identical; default tiled)
@@ -309,6 +425,14 @@ cudaError_t prepare_plan(tt_channel_s* h) {
     const bool want_rw = force && !strcmp(force, "rw");
     const bool want_generic = force && !strcmp(force, "generic");
     if (want_generic) return cudaSuccess;
+    // dense-window kernel: opt-in (TT_KERNEL=dw), wherever it fits. It reads ~3x fewer
+    // x operands from shared memory than the tiled kernel on dense delays, but measured
+    // slower on every BASELINE shape (per-tap dispatch)
+    const bool want_dw = force && !strcmp(force, "dw");
+    if (want_dw) {
+        cudaError_t e = prepare_dw(h);
+        if (e != cudaSuccess) return e;
+    }
     // register-window kernel (R = 16 or 8 consecutive outputs per thread): needs
     // R-aligned snapshot intervals and two window stages of (Hp + T) / R doubled blocks
     const bool want_rw8 = force && !strcmp(force, "rw8");
@@ -321,6 +445,7 @@ cudaError_t prepare_plan(tt_channel_s* h) {
     if ((e = prepare_tiled<false>(h)) != cudaSuccess) return e;
     if ((e = prepare_tiled<true>(h)) != cudaSuccess) return e;
     if (h->plan.rw_smem) h->plan.kind = TT_KERNEL_RW;
+    else if (h->plan.dw.CW && h->plan.tiled[0].R != 0 && h->plan.tiled[1].R != 0) h->plan.kind = TT_KERNEL_DW;
     else if (h->plan.tiled[0].R != 0 || h->plan.tiled[1].R != 0) h->plan.kind = TT_KERNEL_TILED;
     return cudaSuccess;
 }
@@ -381,11 +506,77 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
     p.t_mod = static_cast<int32_t>(h->t % h->S);
     const bool noise = sigma > 0.0f;
     const int nch = c_hi - c_lo;
-    if (h->plan.kind == TT_KERNEL_RW && !ar.agg && !h->in_row && !sparse) {
+    // dense-window kernel: plain calls whose start and length are multiples of 16 (each
+    // thread's 16 outputs then sit in one snapshot interval, and x / y rows are whole
+    // 16-sample TMA rows) on 16-B aligned buffers
+    const bool dw_call = h->plan.kind == TT_KERNEL_DW && !ar.agg && !h->in_row && !sparse && !h->dclock &&
+                         !h->force_robust && h->t % 16 == 0 && n % 16 == 0 &&
+                         (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0 &&
+                         y != nullptr;
+    if (dw_call) {
+        const DwPlan& dp = h->plan.dw;
+        const int T = dp.CW * 32 * tt::dw::R;
+        tt::dw::Params q{};
+        q.ring = h->ring;
+        q.tab = h->dwtab;
+        q.hist_wr = p.hist_wr;
+        q.n = n;
+        q.t = h->t;
+        q.cap = h->cap;
+        q.chan_offset = h->chan_off;
+        q.t_div = p.t_div;
+        q.t_mod = p.t_mod;
+        q.c_lo = c_lo;
+        q.tiles_per_ch = static_cast<int32_t>((n + T - 1) / T);
+        q.total_tiles = static_cast<int64_t>(nch) * q.tiles_per_ch;
+        q.L = h->L;
+        q.L4 = h->L4;
+        q.H = h->H;
+        q.Hw = (h->H + 127) & ~127;
+        q.S = h->S;
+        q.s_shift = p.s_shift;
+        q.inv_S = p.inv_S;
+        q.nk_max = dp.nk_max;
+        q.stages = dp.stages;
+        q.win_rows = dp.win_rows;
+        q.hist_row0 = (h->H - q.Hw) / 16;
+        q.stage_bytes = dp.stage_bytes;
+        q.coef_off = dp.coef_off;
+        q.tab_off = dp.tab_off;
+        q.key0 = p.key0;
+        q.key1 = p.key1;
+        q.noise_sc = p.noise_sc;
+        if (q.total_tiles >= (int64_t(1) << 31)) return fail(TT_ERR_INVALID_ARG, "call too large");
+        CUtensorMap tmx, tmy;
+        if (!encode_rows(&tmx, x, static_cast<uint64_t>(n / 16), static_cast<uint64_t>(nch), tt::dw::kXBoxRows) ||
+            !encode_rows(&tmy, y, static_cast<uint64_t>(n / 16), static_cast<uint64_t>(nch), tt::dw::kXBoxRows))
+            return fail(TT_ERR_CUDA, "cuTensorMapEncodeTiled failed for the input / output buffers");
+        const CUtensorMap& tmh = h->t == 0 ? h->dw_hist[2] : h->dw_hist[h->p];
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+        cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(q.total_tiles, h->num_sms)));
+        cfg.blockDim = dim3((dp.CW + 1) * 32);
+        cfg.dynamicSmemBytes = dp.smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (dp.CW == 8) {
+            if (noise) cudaLaunchKernelEx(&cfg, tt::dw::tt_conv_dw_kernel<8, true>, tmx, tmy, tmh, q);
+            else cudaLaunchKernelEx(&cfg, tt::dw::tt_conv_dw_kernel<8, false>, tmx, tmy, tmh, q);
+        } else if (dp.CW == 7) {
+            if (noise) cudaLaunchKernelEx(&cfg, tt::dw::tt_conv_dw_kernel<7, true>, tmx, tmy, tmh, q);
+            else cudaLaunchKernelEx(&cfg, tt::dw::tt_conv_dw_kernel<7, false>, tmx, tmy, tmh, q);
+        } else {
+            if (noise) cudaLaunchKernelEx(&cfg, tt::dw::tt_conv_dw_kernel<4, true>, tmx, tmy, tmh, q);
+            else cudaLaunchKernelEx(&cfg, tt::dw::tt_conv_dw_kernel<4, false>, tmx, tmy, tmh, q);
+        }
+    } else if (h->plan.kind == TT_KERNEL_RW && !ar.agg && !h->in_row && !sparse) {
         if (h->plan.rw_R == 8) launch_rw<8>(h, p, x, y, c_lo, nch, n, noise, st);
         else launch_rw<16>(h, p, x, y, c_lo, nch, n, noise, st);
     } else if (h->plan.tiled[noise ? 1 : 0].R != 0 &&
-               (h->plan.kind == TT_KERNEL_TILED || ar.agg || h->in_row || sparse)) {
+               (h->plan.kind == TT_KERNEL_TILED || h->plan.kind == TT_KERNEL_DW || ar.agg || h->in_row || sparse)) {
         const TiledPlan& tp = h->plan.tiled[noise ? 1 : 0];
         const int T = tp.CW * 32 * tp.R;
         // a short lead-in tile when the call does not start on a 32R-aligned global
@@ -527,6 +718,7 @@ void free_all(tt_channel_s* h) {
     cudaFree(h->perm);
     cudaFree(h->xoff);
     cudaFree(h->tab);
+    cudaFree(h->dwtab);
     cudaFree(h->dclk);
     cudaFree(h->in_row);
     cudaFree(h->sring);
@@ -639,9 +831,27 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
     if ((e = cudaMalloc(&h->perm, pm_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(perm)"));
     if ((e = cudaMalloc(&h->xoff, xo_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(xoff)"));
     if ((e = cudaMalloc(&h->tab, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(tab)"));
+    {
+        // dense-window tap table: per sorted tap, d = 16 q + f and the block step from the
+        // previous tap (0, 1, or 2 = jump / first tap: read both blocks)
+        std::vector<int32_t> dt(static_cast<size_t>(num_ue) * h->L4, -1);  // pads: -1 ends a block scan
+        for (int c = 0; c < num_ue; ++c) {
+            const int32_t* dc = h->sorted_d.data() + static_cast<size_t>(c) * num_taps;
+            for (int j = 0; j < num_taps; ++j) {
+                const int32_t q = dc[j] >> 4, f = dc[j] & 15;
+                const int32_t dq = j == 0 ? 2 : std::min(2, q - (dc[j - 1] >> 4));
+                dt[static_cast<size_t>(c) * h->L4 + j] = f | (dq << 4) | (q << 8);
+            }
+        }
+        const size_t dt_b = dt.size() * sizeof(int32_t);
+        if ((e = cudaMalloc(&h->dwtab, dt_b)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(dw table)"));
+        if ((e = cudaMemcpy(h->dwtab, dt.data(), dt_b, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return bail(cuda_fail(e, "copy dw table"));
+        h->dev_bytes += dt_b;
+    }
     if ((e = cudaMalloc(&h->dclk, sizeof(tt::DevClock))) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(clock)"));
     if ((e = cudaMemset(h->dclk, 0, sizeof(tt::DevClock))) != cudaSuccess) return bail(cuda_fail(e, "zero clock"));
-    h->dev_bytes = ring_b + hist_b + hist_b / 2 + pm_b + xo_b + tb_b;
+    h->dev_bytes += ring_b + hist_b + hist_b / 2 + pm_b + xo_b + tb_b;
     if ((e = cudaMemset(h->tab, 0, tb_b)) != cudaSuccess) return bail(cuda_fail(e, "zero tab"));
     if ((e = cudaMemcpy(h->perm, pm.data(), pm_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy perm"));
     if ((e = cudaMemcpy(h->xoff, xo.data(), xo_b, cudaMemcpyHostToDevice)) != cudaSuccess) return bail(cuda_fail(e, "copy xoff"));
@@ -1028,7 +1238,8 @@ tt_status tt_channel_set_device_clock(tt_channel_t h, int32_t enable, tt_stream_
     DeviceGuard dg(h->dev);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (enable && !h->dclock) {
-        if (h->plan.kind != TT_KERNEL_TILED || h->plan.tiled[0].R == 0 || h->plan.tiled[1].R == 0)
+        if ((h->plan.kind != TT_KERNEL_TILED && h->plan.kind != TT_KERNEL_DW) || h->plan.tiled[0].R == 0 ||
+            h->plan.tiled[1].R == 0)
             return fail(TT_ERR_UNSUPPORTED, "device-clock mode needs the tiled kernel for this handle's shape");
         const int64_t A = clock_grid(h);
         if (h->t % A != 0)
@@ -1075,8 +1286,10 @@ tt_status tt_channel_get_info(tt_channel_t h, tt_channel_info* info) {
     info->kernel = h->plan.kind;
     info->top_n = h->top_n;
     info->device_clock = h->dclock ? 1 : 0;
-    info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW ? h->plan.rw_R
-                               : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R : 0;
+    info->outputs_per_thread = h->plan.kind == TT_KERNEL_RW    ? h->plan.rw_R
+                               : h->plan.kind == TT_KERNEL_DW    ? tt::dw::R
+                               : h->plan.kind == TT_KERNEL_TILED ? h->plan.tiled[1].R
+                                                                 : 0;
     info->launches_per_apply = h->plan.kind == TT_KERNEL_GENERIC ? 2 : 1;
     return TT_OK;
 }

@@ -187,11 +187,13 @@ def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     for calls that do not start on a 32R-aligned sample or rows off a 16-B boundary; forced
     here with TT_ROBUST=1), the register-window kernels and the generic kernel run the
     same per-output operation sequence: outputs are equal bit for bit, for any call split
-    (history carried across 16-misaligned call starts)."""
+    (history carried across 16-misaligned call starts). The dense-window kernel (forced
+    with TT_KERNEL=dw) runs the calls that start and end on 16-sample multiples and hands
+    the delay line to and from the tiled kernel for the others."""
     w = ttsynth.get(name).scaled(**kw)
     run = Run(w, seed=21)
     outs = {}
-    for k in ("rw", "rw8", "tiled", "generic"):
+    for k in ("rw", "rw8", "tiled", "generic", "dw"):
         monkeypatch.setenv("TT_KERNEL", k)
         outs[k] = run.gpu(cuda_device, calls=calls)
     monkeypatch.setenv("TT_KERNEL", "tiled")
@@ -203,6 +205,7 @@ def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     assert np.array_equal(outs["rw"], outs["tiled"])
     assert np.array_equal(outs["rw8"], outs["tiled"])
     assert np.array_equal(outs["rw"], outs["generic"])
+    assert np.array_equal(outs["dw"], outs["tiled"])
     compare(outs["rw"], run.oracle(), name)
 
 

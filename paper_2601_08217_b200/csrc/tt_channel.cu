@@ -168,6 +168,13 @@ cudaError_t prepare_kernel(size_t budget) {
                           cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, sm)})
         if (e != cudaSuccess) return e;
+    if constexpr (R == 8 && CW == 16) {  // split-warp instances (S = 16R = 128, aligned calls)
+        for (cudaError_t e : {cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false, false, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                              cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, false, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm)})
+            if (e != cudaSuccess) return e;
+    }
     return cudaSuccess;
 }
 
@@ -640,8 +647,22 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         if (robust) TT_LAUNCH_R(RR, CC, true);    \
         else TT_LAUNCH_R(RR, CC, false);          \
     } while (0)
+        // split-warp instance (tt_conv.cuh consume_body): S = 16R, non-robust calls
+        const bool split = !robust && tp.R == 8 && tp.CW == 16 && h->S == 16 * tp.R;
         switch (tp.R * 100 + tp.CW) {
-            case 816: TT_LAUNCH(8, 16); break;
+            case 816:
+                if (split) {
+                    if (noise) {
+                        if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, true, true, false, true>, p);
+                        else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, true, false, false, true>, p);
+                    } else {
+                        if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, false, true, false, true>, p);
+                        else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, false, false, false, true>, p);
+                    }
+                } else {
+                    TT_LAUNCH(8, 16);
+                }
+                break;
             case 1608: TT_LAUNCH(16, 8); break;
             case 808: TT_LAUNCH(8, 8); break;
             case 416: TT_LAUNCH(4, 16); break;

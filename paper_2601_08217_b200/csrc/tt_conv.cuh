@@ -330,13 +330,14 @@ __device__ __forceinline__ void produce_tile(const ConvParams& p, const TileInfo
     }
 }
 
-// One tap for the R outputs this lane owns: gains first, then the packed MACs.
-template <int R>
+// One tap for the R outputs this lane owns (rows RS outputs apart): gains first, then
+// the packed MACs.
+template <int R, int RS = 32>
 __device__ __forceinline__ void mac_tap(const float4 q, const float2* __restrict__ xp, const float (&alpha)[R],
                                         float2 (&A)[R], float2 (&B)[R]) {
     float2 xv[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+    for (int r = 0; r < R; ++r) xv[r] = xp[r * RS];
     const float2 g = make_float2(q.x, q.y);
     const float2 dg = make_float2(q.z, q.w);
     float2 h[R];
@@ -396,10 +397,13 @@ __device__ __forceinline__ void taps_grouped_rt(const ConvParams& p, const float
     else taps_grouped<R, NG, false>(p, cf, xo, xb, alpha, A, B);
 }
 
-// Consumer warp: the 32R outputs of warp `cw` in tile `ti`. GEN: the general variant
-// (group sums, sparse per-interval offsets); the plain variant compiles none of it.
+// Consumer warp of the non-split kernel instances: the 32R outputs of warp `cw` in tile
+// `ti`, lane j owning cw 32R + j + 32 r. GEN: the general variant (group sums, sparse
+// per-interval offsets); the plain variant compiles none of it. (consume_body<RS = 32>
+// computes the same; this copy keeps the code of the instances that never split —
+// c2-c4 — exactly as measured, ptxas schedules the templated form 0.4-1 % slower.)
 template <int R, int CW, bool NOISE, bool GEN>
-__device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
+__device__ __forceinline__ void consume_tile_plain(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
                                              int lane, bool first, float2* aggdst) {
     const int32_t obase = cw * 32 * R + lane;
     if (cw * 32 * R < ti.Tt) {
@@ -582,8 +586,228 @@ __device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo
     }
 }
 
+// Consumer warp: the 32R outputs of warp `cw` in tile `ti`. GEN: the general variant
+// (group sums, sparse per-interval offsets); the plain variant compiles none of it.
+//
+// Lane layout. RS = 32: lane j owns outputs cw 32R + j + 32 r (r < R), so a row is one
+// contiguous 256-B warp access. RS = 16 ("split warp", used when the snapshot period is
+// S = 16R and the warp starts on an interval boundary, e.g. BASELINE c5: S = 128, R = 8):
+// half-warp g = j / 16 owns the S outputs of interval kw0 + g, lane j owning
+// cw 32R + g S + (j mod 16) + 16 r. Every half-warp then sits in one interval, so a tap
+// reads one gain row per lane (the two half-warps' rows in one LDS.128) and the int4
+// tap-offset prefetch of the one-interval path, instead of the grouped path's two gain
+// rows plus a scalar offset per tap; each half-warp's row is a contiguous 128-B access
+// (one wavefront), so the x reads stay conflict-free. Per output the operation sequence
+// is unchanged.
+template <int R, int CW, bool NOISE, bool GEN, int RS>
+__device__ __forceinline__ void consume_body(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
+                                             int lane, bool first, float2* aggdst) {
+    const int32_t obase = RS == 32 ? cw * 32 * R + lane : cw * 32 * R + (lane >> 4) * (16 * R) + (lane & 15);
+    {
+        // per-output interpolation weight alpha = j / S (a multiply when S is a power of
+        // two: then j * (1/S) is exact and equals the correctly rounded quotient)
+        float alpha[R];
+        int32_t kk[R];
+        // outputs past a tail tile's end are computed but never stored; their coefficient
+        // row is clamped into the staged block
+        if (p.s_shift >= 0) {
+            const uint32_t sh = static_cast<uint32_t>(p.s_shift), mask = static_cast<uint32_t>(p.S) - 1u;
+            const float inv_S = p.inv_S;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t jj = static_cast<uint32_t>(ti.j0 + obase + r * RS);
+                kk[r] = min(static_cast<int32_t>(jj >> sh), ti.nk - 1);
+                alpha[r] = __fmul_rn(__uint2float_rn(jj & mask), inv_S);
+            }
+        } else {
+            const float Sf = __int2float_rn(p.S);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t jj = static_cast<uint32_t>(ti.j0 + obase + r * RS);
+                const uint32_t k = jj / static_cast<uint32_t>(p.S);
+                kk[r] = min(static_cast<int32_t>(k), ti.nk - 1);
+                alpha[r] = __fdiv_rn(__uint2float_rn(jj - k * static_cast<uint32_t>(p.S)), Sf);
+            }
+        }
+        float2 A[R], B[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            A[r] = make_float2(0.f, 0.f);
+            B[r] = make_float2(0.f, 0.f);
+        }
+        const float2* xb = st.win + obase;
+        // warp-uniform: are all 32R outputs of this warp in one snapshot interval?
+        const uint32_t wj0 = static_cast<uint32_t>(ti.j0 + cw * 32 * R);
+        const uint32_t kw0 = div_S(p, wj0);
+        const uint32_t kw1 = div_S(p, wj0 + 32 * R - 1);
+        // tap offsets of interval kk: one row per interval when sparse, else the channel's
+        const int32_t xo_row = (GEN && p.xoff_rows) ? p.L4 : 0;
+        if (RS == 16 || kw0 == kw1) {
+            // one interval per lane: this lane's gain row (split warp: its half-warp's
+            // interval, clamped into the staged rows for outputs past a tail tile's end)
+            const int32_t kl = RS == 16 ? min(static_cast<int32_t>(kw0) + (lane >> 4), ti.nk - 1)
+                                        : static_cast<int32_t>(kw0);
+            const float4* cf = st.coef + static_cast<int64_t>(kl) * p.L;
+            const int32_t* xo = st.xo + kl * xo_row;
+            const int4* xo4 = reinterpret_cast<const int4*>(xo);
+            int32_t j = 0;
+            int4 o4 = xo4[0];
+            for (; j + 4 <= p.L; j += 4) {
+                const int4 o = o4;
+                o4 = xo4[(j >> 2) + 1];  // next group's offsets (L4 >= L + 1 keeps this in range)
+                const float4 q0 = cf[j], q1 = cf[j + 1], q2 = cf[j + 2], q3 = cf[j + 3];
+                mac_tap<R, RS>(q0, xb + o.x, alpha, A, B);
+                mac_tap<R, RS>(q1, xb + o.y, alpha, A, B);
+                mac_tap<R, RS>(q2, xb + o.z, alpha, A, B);
+                mac_tap<R, RS>(q3, xb + o.w, alpha, A, B);
+            }
+            for (; j < p.L; ++j) mac_tap<R, RS>(cf[j], xb + xo[j], alpha, A, B);
+        } else if ((R & (R - 1)) == 0 && p.s_shift >= 5 && p.s_shift <= ilog2_c(32 * R) &&
+                   (wj0 & (p.S - 1)) == 0 && ((32 * R) >> p.s_shift) <= 4 &&
+                   static_cast<int32_t>(kw0) + ((32 * R) >> p.s_shift) <= ti.nk) {  // (tail tiles: rows staged)
+            // the warp starts on an interval boundary and spans NG = 32R / S (2 or 4) whole intervals
+            const float4* cf = st.coef + static_cast<int64_t>(kw0) * p.L;
+            const int32_t* xo = st.xo + kw0 * xo_row;
+            if constexpr (GEN) {
+                if (((32 * R) >> p.s_shift) == 2) taps_grouped_rt<R, (R >= 2 ? 2 : 1)>(p, cf, xo, xb, alpha, A, B);
+                else taps_grouped_rt<R, (R >= 4 ? 4 : 1)>(p, cf, xo, xb, alpha, A, B);
+            } else {
+                if (((32 * R) >> p.s_shift) == 2) taps_grouped<R, (R >= 2 ? 2 : 1), false>(p, cf, xo, xb, alpha, A, B);
+                else taps_grouped<R, (R >= 4 ? 4 : 1), false>(p, cf, xo, xb, alpha, A, B);
+            }
+        } else {
+            for (int32_t j = 0; j < p.L; ++j) {
+                const float2* xp = xb + st.xo[j];  // dense: one offset row
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float4 q = st.coef[kk[r] * p.L + j];
+                    const float2 xv = (GEN && xo_row) ? xb[st.xo[kk[r] * xo_row + j] + r * RS] : xp[r * RS];
+                    const float2 h =
+                        __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w), make_float2(q.x, q.y));
+                    A[r] = __ffma2_rn(make_float2(h.x, h.x), xv, A[r]);
+                    B[r] = __ffma2_rn(make_float2(h.y, h.y), xv, B[r]);
+                }
+            }
+        }
+
+        // epilogue: combine, add noise, store
+        float2 out[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[r] = make_float2(__fsub_rn(A[r].x, B[r].y), __fadd_rn(A[r].y, B[r].x));
+        if constexpr (NOISE) {
+            const int64_t nb = p.t + ti.i0 + obase;  // global sample of row 0
+            const uint32_t cg = static_cast<uint32_t>(p.chan_offset + ti.c);
+            const bool even_base = ((p.t + ti.i0) & 1) == 0;  // CTA-uniform
+            if (even_base && (R % 2 == 0)) {
+                const bool ev = (lane & 1) == 0;
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    // even lane: pair of its row-r sample; odd lane: pair of its row-(r+1) sample
+                    const uint64_t m = static_cast<uint64_t>(nb + (ev ? r : r + 1) * RS) >> 1;
+                    const u32x4 q = philox4x32_10(static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32), cg, 0u,
+                                                  p.key0, p.key1);
+                    const uint32_t s0 = ev ? q.c : q.a, s1 = ev ? q.d : q.b;
+                    const uint32_t v0 = __shfl_xor_sync(0xffffffffu, s0, 1);
+                    const uint32_t v1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+                    // select the words first so each lane runs the transform once per sample
+                    float2 wa, wb;
+                    noise_from_words2(ev ? q.a : v0, ev ? q.b : v1, ev ? v0 : q.c, ev ? v1 : q.d, p.noise_sc, wa,
+                                      wb);
+                    out[r] = make_float2(__fadd_rn(out[r].x, wa.x), __fadd_rn(out[r].y, wa.y));
+                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, wb.x), __fadd_rn(out[r + 1].y, wb.y));
+                }
+            } else if constexpr (R % 2 == 0) {
+                // odd tile base: every lane draws its own pair per row (rows two at a time)
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const int64_t n0 = nb + r * RS, n1 = n0 + RS;
+                    const uint64_t m0 = static_cast<uint64_t>(n0) >> 1, m1 = static_cast<uint64_t>(n1) >> 1;
+                    const u32x4 q0 = philox4x32_10(static_cast<uint32_t>(m0), static_cast<uint32_t>(m0 >> 32), cg, 0u,
+                                                   p.key0, p.key1);
+                    const u32x4 q1 = philox4x32_10(static_cast<uint32_t>(m1), static_cast<uint32_t>(m1 >> 32), cg, 0u,
+                                                   p.key0, p.key1);
+                    const bool odd = (n0 & 1) != 0;  // rows are RS (even) apart: same parity
+                    float2 w0, w1;
+                    noise_from_words2(odd ? q0.c : q0.a, odd ? q0.d : q0.b, odd ? q1.c : q1.a, odd ? q1.d : q1.b,
+                                      p.noise_sc, w0, w1);
+                    out[r] = make_float2(__fadd_rn(out[r].x, w0.x), __fadd_rn(out[r].y, w0.y));
+                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, w1.x), __fadd_rn(out[r + 1].y, w1.y));
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int64_t n = nb + r * RS;
+                    const uint64_t m = static_cast<uint64_t>(n) >> 1;
+                    const u32x4 q = philox4x32_10(static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32), cg, 0u,
+                                                  p.key0, p.key1);
+                    const bool odd = (n & 1) != 0;
+                    const float2 wv = noise_from_words(odd ? q.c : q.a, odd ? q.d : q.b, p.noise_sc);
+                    out[r] = make_float2(__fadd_rn(out[r].x, wv.x), __fadd_rn(out[r].y, wv.y));
+                }
+            }
+        }
+        if (p.y) {
+            float2* yc = p.y + static_cast<int64_t>(ti.c - p.c_lo) * p.n + ti.i0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int32_t o = obase + r * RS;
+                if (o < ti.Tt) yc[o] = out[r];
+            }
+        }
+        if (GEN && aggdst) {
+            // running chunk sum in channel order, kept in the destination row itself (each
+            // element is read back only by the thread that wrote it): s = y_first, s += y_k
+            if (first) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * RS;
+                    if (o < ti.Tt) aggdst[o] = out[r];
+                }
+            } else {
+                // all R reads first (independent loads in flight), then the sums
+                float2 v[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * RS;
+                    v[r] = o < ti.Tt ? aggdst[o] : make_float2(0.f, 0.f);
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = obase + r * RS;
+                    if (o < ti.Tt) aggdst[o] = make_float2(__fadd_rn(v[r].x, out[r].x), __fadd_rn(v[r].y, out[r].y));
+                }
+            }
+        }
+    }
+}
+
+// SPLIT: a kernel instance launched only when S = 16R (the host checks); its warps that
+// start on an interval boundary take the split-warp layout. Other instances run
+// consume_tile_plain.
+template <int R, int CW, bool NOISE, bool GEN, bool SPLIT>
+__device__ __forceinline__ void consume_tile(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
+                                             int lane, bool first, float2* aggdst) {
+    if constexpr (!SPLIT) {
+        consume_tile_plain<R, CW, NOISE, GEN>(p, ti, st, cw, lane, first, aggdst);
+    } else {
+        if (cw * 32 * R < ti.Tt) {
+            const uint32_t wj0 = static_cast<uint32_t>(ti.j0 + cw * 32 * R);
+            if ((wj0 & static_cast<uint32_t>(16 * R - 1)) == 0)  // S = 16R
+                consume_body<R, CW, NOISE, GEN, 16>(p, ti, st, cw, lane, first, aggdst);
+            else
+                consume_body<R, CW, NOISE, GEN, 32>(p, ti, st, cw, lane, first, aggdst);
+        }
+        // the tile that ends the call writes the new delay-line history (ping-pong); the
+        // window index of call-local sample n - H + i is Tt + i
+        if (ti.i0 + ti.Tt == p.n) {
+            float2* hw = p.hist_wr + static_cast<int64_t>(ti.c) * p.H;
+            for (int32_t i = cw * 32 + lane; i < p.H; i += CW * 32) hw[i] = st.win[ti.Tt + i];
+        }
+    }
+}
+
 // CW consumer warps + 1 producer warp; tile T = CW x 32 x R outputs of one channel
-template <int R, int CW, bool NOISE, bool GEN, bool ROBUST>
+template <int R, int CW, bool NOISE, bool GEN, bool ROBUST, bool SPLIT>
 // (shapes with <= 8 consumer warps and R <= 8 run two CTAs per SM: independent CTAs drift apart, so
 // one CTA's noise epilogue can overlap the other's tap loop; measured slower, opt-in)
 __device__ __forceinline__ void conv_body(const ConvParams& p) {
@@ -668,7 +892,7 @@ __device__ __forceinline__ void conv_body(const ConvParams& p) {
                 mbar_wait(&full[s], ph);
                 const TileInfo ti =
                     tile_info<R, CW, ROBUST>(p, p.c_lo + static_cast<int32_t>(tw.cl), static_cast<int32_t>(tw.tl));
-                consume_tile<R, CW, NOISE, GEN>(p, ti, shifted(stage(s)), warp, lane, true, nullptr);
+                consume_tile<R, CW, NOISE, GEN, SPLIT>(p, ti, shifted(stage(s)), warp, lane, true, nullptr);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
@@ -681,7 +905,7 @@ __device__ __forceinline__ void conv_body(const ConvParams& p) {
                     // the chunk's sum goes straight into the group row, or into its partial row
                     float2* aggdst =
                         p.agg ? p.agg + (static_cast<int64_t>(si.g) * p.nchunks + si.q) * p.n + ti.i0 : nullptr;
-                    consume_tile<R, CW, NOISE, true>(p, ti, shifted(stage(s)), warp, lane, k == 0, aggdst);
+                    consume_tile<R, CW, NOISE, true, SPLIT>(p, ti, shifted(stage(s)), warp, lane, k == 0, aggdst);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                 }
@@ -692,7 +916,7 @@ __device__ __forceinline__ void conv_body(const ConvParams& p) {
 
 // The tiled kernel. The ROBUST variant can run on the device clock: it waits for the
 // previous grid (PDL) before reading it, and the last CTA to finish advances it.
-template <int R, int CW, bool NOISE, bool GEN, bool ROBUST>
+template <int R, int CW, bool NOISE, bool GEN, bool ROBUST, bool SPLIT = false>
 __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt_conv_kernel(const ConvParams p) {
     if constexpr (ROBUST) {
         ConvParams q = p;
@@ -708,7 +932,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
             q.hist_rd = t == 0 ? p.hist_zero : p.hist_base + par * p.hist_half;
             q.hist_wr = p.hist_base + (par ^ 1) * p.hist_half;
         }
-        conv_body<R, CW, NOISE, GEN, ROBUST>(q);
+        conv_body<R, CW, NOISE, GEN, ROBUST, SPLIT>(q);
         if (p.clk) {
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -722,7 +946,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 8 && R <= 8 ? 2 : 1)) tt
             }
         }
     } else {
-        conv_body<R, CW, NOISE, GEN, ROBUST>(p);
+        conv_body<R, CW, NOISE, GEN, ROBUST, SPLIT>(p);
     }
 }
 

@@ -1,0 +1,250 @@
+// mb_mlp.cu — does the tiled kernel's tap loop need 16 warps per SM to keep the
+// shared-memory pipe busy, and would a software-pipelined loop (next tap's x loaded
+// while the current tap's MACs run) let fewer warps do it? (every way of
+// hiding the noise under the tap loop lost because fewer warps in the loop starve it.)
+//
+// The loop is the product's one-interval path: lane j owns outputs j + 32 r (r < 8), x
+// window in shared memory, 48 taps at the c4-like sorted delays, one broadcast gain row
+// per tap, h = fma(alpha, dg, g), A += h.re x, B += h.im x. One CTA per SM (forced with
+// shared memory), W warps, each running REPS passes over the taps.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb_mlp tools/mb_mlp.cu && ./mb_mlp
+//
+// Prints output-taps per SM-clock (clock64 spans, median over CTAs) per (W, prefetch).
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../paper_2601_08217_b200/csrc/tt_noise.cuh"
+
+constexpr int R = 8, L = 48, WIN = 5120, REPS = 64;
+
+template <int W, int PF, int MAXB>
+__global__ void __launch_bounds__(W * 32, 1) k_loop(const int* __restrict__ dl, float* out, long long* cyc) {
+    extern __shared__ unsigned char sm[];
+    float2* win = reinterpret_cast<float2*>(sm);
+    float4* cf = reinterpret_cast<float4*>(sm + WIN * 8);
+    int* xo = reinterpret_cast<int*>(sm + WIN * 8 + (L + 4) * 16);
+    for (int i = threadIdx.x; i < WIN; i += blockDim.x) win[i] = make_float2(1e-3f * (i % 61), -1e-3f * (i % 53));
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x)
+        cf[i] = make_float4(1e-2f * i, 2e-2f, -1e-3f * i, 1e-3f);
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x) xo[i] = i < L ? 1040 - dl[i] : 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float alpha[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) alpha[r] = (lane + 32 * r) * (1.f / 256);
+    float2 A[R], B[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) A[r] = B[r] = make_float2(0.f, 0.f);
+    const float2* xb0 = win + (warp % 16) * 32 * R + lane;
+    long long t0 = clock64();
+    for (int rep = 0; rep < REPS; ++rep) {
+        const float2* xb = xb0 + ((rep * 7) & 15);  // a different window offset per pass (no hoisting)
+        if constexpr (PF == 0) {
+#pragma unroll 4
+            for (int j = 0; j < L; ++j) {
+                const float4 q = cf[j];
+                const float2* xp = xb + xo[j];
+                float2 xv[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float2 h = __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w),
+                                                make_float2(q.x, q.y));
+                    A[r] = __ffma2_rn(make_float2(h.x, h.x), xv[r], A[r]);
+                    B[r] = __ffma2_rn(make_float2(h.y, h.y), xv[r], B[r]);
+                }
+            }
+        } else {
+            float2 xn[R];
+            float4 qn = cf[0];
+            {
+                const float2* xp = xb + xo[0];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xn[r] = xp[r * 32];
+            }
+#pragma unroll 2
+            for (int j = 0; j < L; ++j) {
+                float2 xv[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xv[r] = xn[r];
+                const float4 q = qn;
+                qn = cf[j + 1];
+                const float2* xp = xb + xo[j + 1];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xn[r] = xp[r * 32];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float2 h = __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w),
+                                                make_float2(q.x, q.y));
+                    A[r] = __ffma2_rn(make_float2(h.x, h.x), xv[r], A[r]);
+                    B[r] = __ffma2_rn(make_float2(h.y, h.y), xv[r], B[r]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s += A[r].x + A[r].y + B[r].x + B[r].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// WL loop warps (the tap loop above, no prefetch) next to WN noise warps that draw
+// Philox4x32-10 + the packed tt-normal-v1 transform (two samples per call) in a loop.
+// Reports the loop warps' output-taps per clock and the noise warps' samples per clock,
+// each over its own span.
+template <int WL, int WN>
+__global__ void __launch_bounds__((WL + WN) * 32, 1) k_mixed(const int* __restrict__ dl, float* out, long long* cyc,
+                                                            int noise_iters) {
+    extern __shared__ unsigned char sm[];
+    float2* win = reinterpret_cast<float2*>(sm);
+    float4* cf = reinterpret_cast<float4*>(sm + WIN * 8);
+    int* xo = reinterpret_cast<int*>(sm + WIN * 8 + (L + 4) * 16);
+    for (int i = threadIdx.x; i < WIN; i += blockDim.x) win[i] = make_float2(1e-3f * (i % 61), -1e-3f * (i % 53));
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x)
+        cf[i] = make_float4(1e-2f * i, 2e-2f, -1e-3f * i, 1e-3f);
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x) xo[i] = i < L ? 1040 - dl[i] : 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long t0 = clock64();
+    float s = 0;
+    if (warp < WL) {
+        float alpha[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) alpha[r] = (lane + 32 * r) * (1.f / 256);
+        float2 A[R], B[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) A[r] = B[r] = make_float2(0.f, 0.f);
+        const float2* xb0 = win + (warp % 16) * 32 * R + lane;
+        for (int rep = 0; rep < REPS; ++rep) {
+            const float2* xb = xb0 + ((rep * 7) & 15);
+#pragma unroll 4
+            for (int j = 0; j < L; ++j) {
+                const float4 q = cf[j];
+                const float2* xp = xb + xo[j];
+                float2 xv[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float2 h = __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w),
+                                                make_float2(q.x, q.y));
+                    A[r] = __ffma2_rn(make_float2(h.x, h.x), xv[r], A[r]);
+                    B[r] = __ffma2_rn(make_float2(h.y, h.y), xv[r], B[r]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) s += A[r].x + A[r].y + B[r].x + B[r].y;
+    } else {
+        float2 acc = make_float2(0.f, 0.f);
+        for (int it = 0; it < noise_iters; ++it) {
+            const uint32_t m = static_cast<uint32_t>(it * 1024 + threadIdx.x);
+            const tt::u32x4 q = tt::philox4x32_10(m, 0u, blockIdx.x, 0u, 0x1234u, 0x5678u);
+            float2 w0, w1;
+            tt::noise_from_words2(q.a, q.b, q.c, q.d, 0.3f, w0, w1);
+            acc.x += w0.x + w1.x;
+            acc.y += w0.y + w1.y;
+        }
+        s = acc.x + acc.y;
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (lane == 0) cyc[blockIdx.x * 64 + warp] = t1 - t0;
+}
+
+template <int WL, int WN>
+int run_mixed(const int* dl, float* out, long long* cyc, int sms, int noise_iters) {
+    auto k = k_mixed<WL, WN>;
+    const int smem = 200 * 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int i = 0; i < 2; ++i) k<<<sms, (WL + WN) * 32, smem>>>(dl, out, cyc, noise_iters);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+    std::vector<long long> h(sms * 64);
+    cudaMemcpy(h.data(), cyc, sizeof(long long) * sms * 64, cudaMemcpyDeviceToHost);
+    std::vector<long long> lc, nc;
+    for (int b = 0; b < sms; ++b) {
+        long long ml = 0, mn = 0;
+        for (int w = 0; w < WL; ++w) ml = std::max(ml, h[b * 64 + w]);
+        for (int w = WL; w < WL + WN; ++w) mn = std::max(mn, h[b * 64 + w]);
+        lc.push_back(ml);
+        nc.push_back(mn);
+    }
+    std::sort(lc.begin(), lc.end());
+    std::sort(nc.begin(), nc.end());
+    const double ot = (double)WL * 32 * R * L * REPS;
+    const double ns = (double)WN * 32 * 2 * noise_iters;
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    printf(",\n{\"loop_warps\": %d, \"noise_warps\": %d, \"noise_iters\": %d, \"regs\": %d, \"loop_outtaps_per_clk\": %.3f, "
+           "\"loop_cycles\": %.0f, \"noise_samples_per_clk\": %.3f, \"noise_cycles\": %.0f}",
+           WL, WN, noise_iters, fa.numRegs, ot / lc[sms / 2], (double)lc[sms / 2], WN ? ns / nc[sms / 2] : 0.0,
+           (double)nc[sms / 2]);
+    return 0;
+}
+
+template <int W, int PF>
+int run(const int* dl, float* out, long long* cyc, int sms) {
+    auto k = k_loop<W, PF, 1>;
+    const int smem = 200 * 1024;  // one CTA per SM
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int i = 0; i < 2; ++i) k<<<sms, W * 32, smem>>>(dl, out, cyc);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+    std::vector<long long> h(sms);
+    cudaMemcpy(h.data(), cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    std::sort(h.begin(), h.end());
+    const double c = (double)h[sms / 2];
+    const double ot = (double)W * 32 * R * L * REPS;
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    printf("%s{\"warps\": %d, \"prefetch\": %d, \"regs\": %d, \"outtaps_per_clk_per_sm\": %.3f}", W == 4 && PF == 0 ? "" : ",\n",
+           W, PF, fa.numRegs, ot / c);
+    return 0;
+}
+
+int main() {
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, 0);
+    const int sms = prop.multiProcessorCount;
+    std::vector<int> hd(L);
+    for (int i = 0; i < L; ++i) hd[i] = i == 0 ? 0 : (i * 977 + 13) % 1024;
+    std::sort(hd.begin(), hd.end());
+    int* dl;
+    float* out;
+    long long* cyc;
+    cudaMalloc(&dl, L * sizeof(int));
+    cudaMemcpy(dl, hd.data(), L * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMalloc(&out, sizeof(float) * sms * 1024);
+    cudaMalloc(&cyc, sizeof(long long) * sms * 64);
+    printf("[\n");
+    run<4, 0>(dl, out, cyc, sms);
+    run<4, 1>(dl, out, cyc, sms);
+    run<8, 0>(dl, out, cyc, sms);
+    run<8, 1>(dl, out, cyc, sms);
+    run<12, 0>(dl, out, cyc, sms);
+    run<12, 1>(dl, out, cyc, sms);
+    run<16, 0>(dl, out, cyc, sms);
+    run<16, 1>(dl, out, cyc, sms);
+    run<20, 0>(dl, out, cyc, sms);
+    run<24, 0>(dl, out, cyc, sms);
+    run<32, 0>(dl, out, cyc, sms);
+    // the noise alone, then beside the loop: c4 needs one noise sample per 48 output-taps,
+    // i.e. per loop warp pass (REPS x 48 taps x 256 outputs) 256 x REPS samples = 128 REPS
+    // two-sample calls per 32 lanes -> noise_iters = 128 REPS / 32 per noise lane per loop warp
+    run_mixed<0, 4>(dl, out, cyc, sms, 512);
+    run_mixed<16, 0>(dl, out, cyc, sms, 0);
+    run_mixed<12, 4>(dl, out, cyc, sms, 4 * REPS * 12 / 4);
+    run_mixed<16, 4>(dl, out, cyc, sms, 4 * REPS * 16 / 4);
+    run_mixed<8, 8>(dl, out, cyc, sms, 4 * REPS * 8 / 8);
+    run_mixed<12, 8>(dl, out, cyc, sms, 4 * REPS * 12 / 8);
+    run_mixed<16, 8>(dl, out, cyc, sms, 4 * REPS * 16 / 8);
+    printf("\n]\n");
+    return 0;
+}

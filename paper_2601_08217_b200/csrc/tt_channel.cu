@@ -66,7 +66,7 @@ struct TiledPlan {
     size_t smem = 0;     // dynamic shared memory bytes
     int nk_max = 0;      // gain rows staged per tile
 };
-// dense-window kernel (tt_conv_dw.cuh): chosen for taps dense in delay
+// dense-window kernel (tt_conv_dw.cuh; opt-in, TT_KERNEL=dw)
 struct DwPlan {
     int CW = 0;            // consumer warps (0: not planned)
     int stages = 0;

@@ -190,6 +190,107 @@ int run_mixed(const int* dl, float* out, long long* cyc, int sms, int noise_iter
     return 0;
 }
 
+// Gain-read variants of the 16-warp loop (int4 offset prefetch as in the product):
+// G = 0: one LDS.128 broadcast per tap (the product); 1: two LDS.64 broadcasts;
+// 2: no gain read (loop-invariant registers: the upper bound); 3: LDG through L1
+// (the gain rows in global memory, all lanes the same address).
+template <int G>
+__global__ void __launch_bounds__(16 * 32, 1) k_gain(const int* __restrict__ dl, const float4* __restrict__ gcf,
+                                                      float* out, long long* cyc) {
+    extern __shared__ unsigned char sm[];
+    float2* win = reinterpret_cast<float2*>(sm);
+    float4* cf = reinterpret_cast<float4*>(sm + WIN * 8);
+    int* xo = reinterpret_cast<int*>(sm + WIN * 8 + (L + 4) * 16);
+    for (int i = threadIdx.x; i < WIN; i += blockDim.x) win[i] = make_float2(1e-3f * (i % 61), -1e-3f * (i % 53));
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x)
+        cf[i] = make_float4(1e-2f * i, 2e-2f, -1e-3f * i, 1e-3f);
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x) xo[i] = i < L ? 1040 - dl[i] : 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float alpha[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) alpha[r] = (lane + 32 * r) * (1.f / 256);
+    float2 A[R], B[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) A[r] = B[r] = make_float2(0.f, 0.f);
+    const float2* xb0 = win + (warp % 16) * 32 * R + lane;
+    const float4 qc = make_float4(0.01f * lane, 0.02f, -0.001f, 0.001f * warp);
+    // G = 4: lane l holds taps l and l + 32 (registers), broadcast per tap by 4 SHFL
+    const float4 ql0 = cf[lane], ql1 = cf[(lane + 32) % (L + 4)];
+    long long t0 = clock64();
+    for (int rep = 0; rep < REPS; ++rep) {
+        const float2* xb = xb0 + ((rep * 7) & 15);
+        const int4* xo4 = reinterpret_cast<const int4*>(xo);
+        int4 o4 = xo4[0];
+        for (int j = 0; j < L; j += 4) {
+            const int4 o = o4;
+            o4 = xo4[(j >> 2) + 1];
+            float4 qs[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if constexpr (G == 0) qs[t] = cf[j + t];
+                else if constexpr (G == 1) {
+                    const float2 a = reinterpret_cast<const float2*>(cf)[2 * (j + t)];
+                    const float2 b = reinterpret_cast<const float2*>(cf)[2 * (j + t) + 1];
+                    qs[t] = make_float4(a.x, a.y, b.x, b.y);
+                } else if constexpr (G == 2) qs[t] = make_float4(qc.x + t, qc.y, qc.z, qc.w);
+                else if constexpr (G == 3) qs[t] = __ldg(gcf + ((j + t + rep) & 63));
+                else if constexpr (G == 4) {
+                    const int jj = j + t;
+                    const float4 src = jj < 32 ? ql0 : ql1;
+                    qs[t] = make_float4(__shfl_sync(0xffffffffu, src.x, jj & 31), __shfl_sync(0xffffffffu, src.y, jj & 31),
+                                        __shfl_sync(0xffffffffu, src.z, jj & 31), __shfl_sync(0xffffffffu, src.w, jj & 31));
+                } else {  // G == 5: lane 0 reads, 4 SHFL broadcast
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (lane == 0) v = cf[j + t];
+                    qs[t] = make_float4(__shfl_sync(0xffffffffu, v.x, 0), __shfl_sync(0xffffffffu, v.y, 0),
+                                        __shfl_sync(0xffffffffu, v.z, 0), __shfl_sync(0xffffffffu, v.w, 0));
+                }
+            }
+            const int offs[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float4 q = qs[t];
+                const float2* xp = xb + offs[t];
+                float2 xv[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float2 h = __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w),
+                                                make_float2(q.x, q.y));
+                    A[r] = __ffma2_rn(make_float2(h.x, h.x), xv[r], A[r]);
+                    B[r] = __ffma2_rn(make_float2(h.y, h.y), xv[r], B[r]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s += A[r].x + A[r].y + B[r].x + B[r].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int G>
+int run_gain(const int* dl, const float4* gcf, float* out, long long* cyc, int sms) {
+    auto k = k_gain<G>;
+    const int smem = 200 * 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int i = 0; i < 2; ++i) k<<<sms, 16 * 32, smem>>>(dl, gcf, out, cyc);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+    std::vector<long long> h(sms);
+    cudaMemcpy(h.data(), cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    std::sort(h.begin(), h.end());
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    printf(",\n{\"gain_read\": %d, \"regs\": %d, \"outtaps_per_clk_per_sm\": %.3f}", G, fa.numRegs,
+           (double)16 * 32 * R * L * REPS / h[sms / 2]);
+    return 0;
+}
+
 template <int W, int PF>
 int run(const int* dl, float* out, long long* cyc, int sms) {
     auto k = k_loop<W, PF, 1>;
@@ -235,6 +336,15 @@ int main() {
     run<20, 0>(dl, out, cyc, sms);
     run<24, 0>(dl, out, cyc, sms);
     run<32, 0>(dl, out, cyc, sms);
+    float4* gcf;
+    cudaMalloc(&gcf, 64 * sizeof(float4));
+    cudaMemset(gcf, 0, 64 * sizeof(float4));
+    run_gain<0>(dl, gcf, out, cyc, sms);
+    run_gain<1>(dl, gcf, out, cyc, sms);
+    run_gain<2>(dl, gcf, out, cyc, sms);
+    run_gain<3>(dl, gcf, out, cyc, sms);
+    run_gain<4>(dl, gcf, out, cyc, sms);
+    run_gain<5>(dl, gcf, out, cyc, sms);
     // the noise alone, then beside the loop: c4 needs one noise sample per 48 output-taps,
     // i.e. per loop warp pass (REPS x 48 taps x 256 outputs) 256 x REPS samples = 128 REPS
     // two-sample calls per 32 lanes -> noise_iters = 128 REPS / 32 per noise lane per loop warp

@@ -168,10 +168,14 @@ cudaError_t prepare_kernel(size_t budget) {
                           cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, sm)})
         if (e != cudaSuccess) return e;
-    if constexpr (R == 8 && CW == 16) {  // split-warp instances (S = 16R = 128, aligned calls)
+    if constexpr (R == 8 && CW == 16) {  // split-warp instances (S = 16R = 128), plain and robust
         for (cudaError_t e : {cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false, false, true>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                               cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, false, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                              cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, false, true, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                              cudaFuncSetAttribute(tt::tt_conv_kernel<R, CW, NOISE, true, true, true>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sm)})
             if (e != cudaSuccess) return e;
     }
@@ -647,21 +651,24 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         if (robust) TT_LAUNCH_R(RR, CC, true);    \
         else TT_LAUNCH_R(RR, CC, false);          \
     } while (0)
-        // split-warp instance (tt_conv.cuh consume_body): S = 16R, non-robust calls
-        const bool split = !robust && tp.R == 8 && tp.CW == 16 && h->S == 16 * tp.R;
+        // split-warp instances (tt_conv.cuh consume_body): S = 16R; in the robust variant
+        // the tiles after the lead-in start on the 32R grid, so their warps split too
+        const bool split = tp.R == 8 && tp.CW == 16 && h->S == 16 * tp.R;
+#define TT_LAUNCH_SPLIT(RB)                                                                          \
+    do {                                                                                             \
+        if (noise) {                                                                                 \
+            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, true, true, RB, true>, p);   \
+            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, true, false, RB, true>, p);      \
+        } else {                                                                                     \
+            if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, false, true, RB, true>, p);  \
+            else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, false, false, RB, true>, p);     \
+        }                                                                                            \
+    } while (0)
         switch (tp.R * 100 + tp.CW) {
             case 816:
-                if (split) {
-                    if (noise) {
-                        if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, true, true, false, true>, p);
-                        else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, true, false, false, true>, p);
-                    } else {
-                        if (gen) cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, false, true, false, true>, p);
-                        else cudaLaunchKernelEx(&cfg, tt::tt_conv_kernel<8, 16, false, false, false, true>, p);
-                    }
-                } else {
-                    TT_LAUNCH(8, 16);
-                }
+                if (split && robust) TT_LAUNCH_SPLIT(true);
+                else if (split) TT_LAUNCH_SPLIT(false);
+                else TT_LAUNCH(8, 16);
                 break;
             case 1608: TT_LAUNCH(16, 8); break;
             case 808: TT_LAUNCH(8, 8); break;
@@ -670,6 +677,7 @@ tt_status launch(tt_channel_s* h, const float2* x, float2* y, int32_t c_lo, int3
         }
 #undef TT_LAUNCH
 #undef TT_LAUNCH_R
+#undef TT_LAUNCH_SPLIT
         if (ar.agg && nchunks > 1) {
             const int64_t tot = static_cast<int64_t>(ngroups) * n;
             const int64_t gg = std::min<int64_t>((tot + 255) / 256, int64_t(h->num_sms) * 8);

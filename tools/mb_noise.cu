@@ -16,9 +16,9 @@
 
 #include "../paper_2601_08217_b200/csrc/tt_noise.cuh"
 
-constexpr int R = 8, ITERS = 256;
+constexpr int ITERS = 256;
 
-template <int W, int V>
+template <int W, int V, int R = 8>
 __global__ void __launch_bounds__(W * 32, 1) k_noise(float* out, long long* cyc, float sc) {
     const int lane = threadIdx.x & 31;
     const bool ev = (lane & 1) == 0;
@@ -94,9 +94,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_noise(float* out, long long* cyc,
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int W, int V>
+template <int W, int V, int R = 8>
 void run(float* out, long long* cyc, int sms, bool first) {
-    auto k = k_noise<W, V>;
+    auto k = k_noise<W, V, R>;
     const int smem = 200 * 1024;  // one CTA per SM
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int i = 0; i < 2; ++i) k<<<sms, W * 32, smem>>>(out, cyc, 0.2236f);
@@ -106,8 +106,8 @@ void run(float* out, long long* cyc, int sms, bool first) {
     std::sort(h.begin(), h.end());
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k);
-    printf("%s{\"warps\": %d, \"variant\": %d, \"regs\": %d, \"samples_per_clk_per_sm\": %.3f}", first ? "" : ",\n", W,
-           V, fa.numRegs, (double)W * 32 * R * ITERS / h[sms / 2]);
+    printf("%s{\"warps\": %d, \"variant\": %d, \"rows\": %d, \"regs\": %d, \"samples_per_clk_per_sm\": %.3f}",
+           first ? "" : ",\n", W, V, R, fa.numRegs, (double)W * 32 * R * ITERS / h[sms / 2]);
 }
 
 int main() {
@@ -125,6 +125,10 @@ int main() {
     run<16, 1>(out, cyc, sms, false);
     run<16, 2>(out, cyc, sms, false);
     run<32, 0>(out, cyc, sms, false);
+    run<8, 0, 16>(out, cyc, sms, false);
+    run<8, 1, 16>(out, cyc, sms, false);
+    run<8, 1>(out, cyc, sms, false);
+    run<12, 1, 16>(out, cyc, sms, false);
     printf("\n]\n");
     return 0;
 }

@@ -93,3 +93,45 @@ def test_max_call_length_and_stream_past_2_pow_32(cuda_device):
             assert rel <= REL_L2 and mabs <= MAX_ABS_RMS, (s, c, rel, mabs)
             worst = (max(worst[0], rel), max(worst[1], mabs))
     print(f"max sizes: {len(starts)} windows up to t = {N}, worst rel L2 {worst[0]:.2e}, max-abs/RMS {worst[1]:.2e}")
+
+
+def test_many_channels_with_global_ids_past_2_pow_32(cuda_device):
+    """65,536 channels in one handle whose global ids (channel_offset + c) wrap past 2^32:
+    the noise key is the global id mod 2^32 on both sides (docs/tt-normal-v1.md §1), and
+    the per-channel offsets into the ring, history and buffers are 64-bit. Two streamed
+    calls; sampled channels (first, around the wrap, last, random) vs the oracle."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    rng = np.random.default_rng(2026)
+    C, L, D, S = 1 << 16, 16, 200, 256
+    calls = [2048, 1536]
+    N = sum(calls)
+    K = (N - 1) // S + 2
+    off = (1 << 32) - 30_000
+    d = np.concatenate([np.zeros((C, 1), np.int64), np.sort(rng.integers(1, D + 1, size=(C, L - 1)), axis=1)],
+                       axis=1).astype(np.int32)
+    g = (rng.standard_normal((C, K, L, 2)) * np.sqrt(0.5 / L)).astype(np.float32)
+    x = (rng.standard_normal((C, N, 2)) * np.sqrt(0.5)).astype(np.float32)
+    sigma = 0.1
+    ys = []
+    with Channel(d, S, seed=5, snapshot_capacity=K, channel_offset=off, device=cuda_device) as ch:
+        ch.load_snapshots(torch.from_numpy(g).to(cuda_device), 0)
+        pos = 0
+        for n in calls:
+            ys.append(ch.apply(torch.from_numpy(np.ascontiguousarray(x[:, pos:pos + n])).to(cuda_device),
+                               noise_sigma=sigma).cpu().numpy())
+            pos += n
+        torch.cuda.synchronize()
+    y = np.concatenate(ys, axis=1)
+    wrap = (1 << 32) - off
+    chans = sorted({0, 1, wrap - 2, wrap - 1, wrap, wrap + 1, C - 1, *(int(c) for c in rng.integers(0, C, 4))})
+    for c in chans:
+        ref = oracle.convolve(d[c:c + 1], S, g[c:c + 1], 0, x[c:c + 1], 0, 0, N, sigma=sigma, seed=5,
+                              c_offset=off + c)[0]
+        yg = y[c, :, 0].astype(np.float64) + 1j * y[c, :, 1]
+        nrm = np.linalg.norm(ref)
+        err = yg - ref
+        assert np.linalg.norm(err) / nrm <= REL_L2, c
+        assert np.abs(err).max() / (nrm / np.sqrt(N)) <= MAX_ABS_RMS, c

@@ -160,6 +160,111 @@ __global__ void __launch_bounds__((WL + WN) * 32, 1) k_mixed(const int* __restri
     if (lane == 0) cyc[blockIdx.x * 64 + warp] = t1 - t0;
 }
 
+// WL loop warps next to WD warps running a side workload: MODE 0 = dependent-chain-free
+// DFMA (FP64 pipe), MODE 1 = Philox4x32-10 only (IMAD.WIDE / LOP3), MODE 2 = FFMA2 only.
+template <int WL, int WD, int MODE>
+__global__ void __launch_bounds__((WL + WD) * 32, 1) k_side(const int* __restrict__ dl, float* out, long long* cyc,
+                                                           int side_iters) {
+    extern __shared__ unsigned char sm[];
+    float2* win = reinterpret_cast<float2*>(sm);
+    float4* cf = reinterpret_cast<float4*>(sm + WIN * 8);
+    int* xo = reinterpret_cast<int*>(sm + WIN * 8 + (L + 4) * 16);
+    for (int i = threadIdx.x; i < WIN; i += blockDim.x) win[i] = make_float2(1e-3f * (i % 61), -1e-3f * (i % 53));
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x)
+        cf[i] = make_float4(1e-2f * i, 2e-2f, -1e-3f * i, 1e-3f);
+    for (int i = threadIdx.x; i < L + 4; i += blockDim.x) xo[i] = i < L ? 1040 - dl[i] : 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long t0 = clock64();
+    float s = 0;
+    if (warp < WL) {
+        float alpha[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) alpha[r] = (lane + 32 * r) * (1.f / 256);
+        float2 A[R], B[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) A[r] = B[r] = make_float2(0.f, 0.f);
+        const float2* xb0 = win + (warp % 16) * 32 * R + lane;
+        for (int rep = 0; rep < REPS; ++rep) {
+            const float2* xb = xb0 + ((rep * 7) & 15);
+#pragma unroll 4
+            for (int j = 0; j < L; ++j) {
+                const float4 q = cf[j];
+                const float2* xp = xb + xo[j];
+                float2 xv[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xv[r] = xp[r * 32];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float2 h = __ffma2_rn(make_float2(alpha[r], alpha[r]), make_float2(q.z, q.w),
+                                                make_float2(q.x, q.y));
+                    A[r] = __ffma2_rn(make_float2(h.x, h.x), xv[r], A[r]);
+                    B[r] = __ffma2_rn(make_float2(h.y, h.y), xv[r], B[r]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) s += A[r].x + A[r].y + B[r].x + B[r].y;
+    } else if constexpr (MODE == 0) {
+        double a[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = 1e-3 * (threadIdx.x + i);
+        for (int it = 0; it < side_iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = fma(a[i], 0.999999, 1e-7);
+        }
+        for (int i = 0; i < 8; ++i) s += static_cast<float>(a[i]);
+    } else if constexpr (MODE == 1) {
+        uint32_t acc = 0;
+        for (int it = 0; it < side_iters; ++it) {
+            const tt::u32x4 q = tt::philox4x32_10(static_cast<uint32_t>(it * 1024 + threadIdx.x), 0u, blockIdx.x, 0u,
+                                                  0x1234u, 0x5678u);
+            acc ^= q.a ^ q.b ^ q.c ^ q.d;
+        }
+        s = static_cast<float>(acc);
+    } else {
+        float2 a[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = make_float2(1e-3f * (threadIdx.x + i), 1e-3f * i);
+        for (int it = 0; it < side_iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(a[i], make_float2(0.9999f, 0.9999f), make_float2(1e-7f, 1e-7f));
+        }
+        for (int i = 0; i < 8; ++i) s += a[i].x + a[i].y;
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (lane == 0) cyc[blockIdx.x * 64 + warp] = t1 - t0;
+}
+
+template <int WL, int WD, int MODE>
+int run_side(const int* dl, float* out, long long* cyc, int sms, int side_iters) {
+    auto k = k_side<WL, WD, MODE>;
+    const int smem = 200 * 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int i = 0; i < 2; ++i) k<<<sms, (WL + WD) * 32, smem>>>(dl, out, cyc, side_iters);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+    std::vector<long long> h(sms * 64);
+    cudaMemcpy(h.data(), cyc, sizeof(long long) * sms * 64, cudaMemcpyDeviceToHost);
+    std::vector<long long> lc, nc;
+    for (int b = 0; b < sms; ++b) {
+        long long ml = 0, mn = 0;
+        for (int w = 0; w < WL; ++w) ml = std::max(ml, h[b * 64 + w]);
+        for (int w = WL; w < WL + WD; ++w) mn = std::max(mn, h[b * 64 + w]);
+        lc.push_back(ml);
+        nc.push_back(mn);
+    }
+    std::sort(lc.begin(), lc.end());
+    std::sort(nc.begin(), nc.end());
+    // side ops per clock per SM: MODE 0: DFMA lanes; 1: Philox calls (x32 lanes); 2: FFMA2 lanes (x2)
+    const double ops = (double)WD * 32 * side_iters * (MODE == 1 ? 1 : 8) * (MODE == 2 ? 2 : 1);
+    printf(",\n{\"side_mode\": %d, \"loop_warps\": %d, \"side_warps\": %d, \"loop_outtaps_per_clk\": %.3f, "
+           "\"side_ops_per_clk\": %.3f, \"loop_cycles\": %.0f, \"side_cycles\": %.0f}",
+           MODE, WL, WD, WL ? (double)WL * 32 * R * L * REPS / lc[sms / 2] : 0.0, WD ? ops / nc[sms / 2] : 0.0,
+           (double)lc[sms / 2], (double)nc[sms / 2]);
+    return 0;
+}
+
 template <int WL, int WN>
 int run_mixed(const int* dl, float* out, long long* cyc, int sms, int noise_iters) {
     auto k = k_mixed<WL, WN>;
@@ -345,6 +450,13 @@ int main() {
     run_gain<3>(dl, gcf, out, cyc, sms);
     run_gain<4>(dl, gcf, out, cyc, sms);
     run_gain<5>(dl, gcf, out, cyc, sms);
+    // side workloads alone, then next to 12 loop warps (iterations sized to ~1 M cycles)
+    run_side<0, 4, 0>(dl, out, cyc, sms, 8192);
+    run_side<12, 4, 0>(dl, out, cyc, sms, 8192);
+    run_side<0, 4, 1>(dl, out, cyc, sms, 4096);
+    run_side<12, 4, 1>(dl, out, cyc, sms, 4096);
+    run_side<0, 4, 2>(dl, out, cyc, sms, 8192);
+    run_side<12, 4, 2>(dl, out, cyc, sms, 8192);
     // the noise alone, then beside the loop: c4 needs one noise sample per 48 output-taps,
     // i.e. per loop warp pass (REPS x 48 taps x 256 outputs) 256 x REPS samples = 128 REPS
     // two-sample calls per 32 lanes -> noise_iters = 128 REPS / 32 per noise lane per loop warp

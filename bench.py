@@ -292,7 +292,11 @@ def main():
     # one-call config (c1, c2, c5) repeats its single call, the stream reset (t = 0, zero
     # delay line) inside each step
     one_shot = w.calls == 1
-    K = (n - 1) // w.S + 2 if one_shot else (steps_total * n - 1) // w.S + 2
+    # a streaming config runs its `calls` slots (c4: 100 slots = 50 ms of air time) and then
+    # starts over (stream reset: t = 0, zero delay line; no device work), so the snapshots
+    # preloaded for it cover at most `calls` slots however long the run
+    slots = 1 if one_shot else min(steps_total, w.calls)
+    K = (slots * n - 1) // w.S + 2
     delays = ttsynth.delays(w, c_lo, c_hi)
     gains = ttsynth.snapshots(w, c_lo, c_hi, K, backend="torch", device=dev)
     slot_bytes = C * n * 8
@@ -308,9 +312,16 @@ def main():
     sigma = w.sigma if args.sigma is None else args.sigma
 
     # ---- device-resident timed region ----------------------------------------------
-    def step(xin):
-        if one_shot:
+    slot = [0]  # slots applied since the last stream reset
+
+    def start_slot():
+        if slot[0] == slots:
             ch.reset()
+            slot[0] = 0
+        slot[0] += 1
+
+    def step(xin):
+        start_slot()
         ch.apply(xin, out=y, noise_sigma=sigma)
 
     for i in range(args.warmup):
@@ -336,16 +347,14 @@ def main():
     if args.e2e_steps > 0:
         xh = [xs[i % P].cpu().pin_memory() for i in range(min(P, 2))]
         yh = torch.empty_like(xh[0]).pin_memory()
-        if one_shot:
-            ch.reset()
+        start_slot()
         ch.apply_host(xh[0], yh, noise_sigma=sigma)  # staging allocation + warm-up
         torch.cuda.synchronize()
         shard.barrier(pg)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.e2e_steps):
-            if one_shot:
-                ch.reset()
+            start_slot()
             ch.apply_host(xh[i % len(xh)], yh, noise_sigma=sigma)
         e1.record(stream)
         torch.cuda.synchronize()

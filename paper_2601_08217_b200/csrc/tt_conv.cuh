@@ -49,6 +49,17 @@ constexpr int kMaxStages = 4;
 #ifndef TT_V
 #define TT_V 0  // kernel variant hook for A/B builds (tools/build_variants.sh); 0 = the product
 #endif
+// The noise add stays two scalar __fadd_rn: ptxas contracts an FMUL2 feeding an FADD2
+// into one FFMA2 even with .rn (checked in SASS), which would fuse the noise scaling
+// w = (rho (cos, sin)) sc into the add and change the rounding.
+__device__ __forceinline__ float2 add_noise(float2 a, float2 w) {
+    return make_float2(__fadd_rn(a.x, w.x), __fadd_rn(a.y, w.y));
+}
+// y = A + i B for A = sum h.re x, B = sum h.im x: (A.x - B.y, A.y + B.x) as one FFMA2
+// with exact +-1 products, per component the rounding of __fsub_rn / __fadd_rn.
+__device__ __forceinline__ float2 combine(float2 a, float2 b) {
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a);
+}
 
 // Stream position kept in device memory (tt_channel_set_device_clock): the kernel
 // reads t and the history parity at its start and its last CTA advances them, so a
@@ -401,7 +412,7 @@ __device__ __forceinline__ void taps_grouped_rt(const ConvParams& p, const float
 // `ti`, lane j owning cw 32R + j + 32 r. GEN: the general variant (group sums, sparse
 // per-interval offsets); the plain variant compiles none of it. (consume_body<RS = 32>
 // computes the same; this copy keeps the code of the instances that never split —
-// c2-c4 — exactly as measured, ptxas schedules the templated form 0.4-1 % slower.)
+// c2-c4 — as measured, ptxas schedules the templated form 0.4-1 % slower.)
 template <int R, int CW, bool NOISE, bool GEN>
 __device__ __forceinline__ void consume_tile_plain(const ConvParams& p, const TileInfo& ti, const Stage& st, int cw,
                                              int lane, bool first, float2* aggdst) {
@@ -492,7 +503,7 @@ __device__ __forceinline__ void consume_tile_plain(const ConvParams& p, const Ti
         // epilogue: combine, add noise, store
         float2 out[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) out[r] = make_float2(__fsub_rn(A[r].x, B[r].y), __fadd_rn(A[r].y, B[r].x));
+        for (int r = 0; r < R; ++r) out[r] = combine(A[r], B[r]);
         if constexpr (NOISE) {
             const int64_t nb = p.t + ti.i0 + obase;  // global sample of row 0
             const uint32_t cg = static_cast<uint32_t>(p.chan_offset + ti.c);
@@ -512,8 +523,8 @@ __device__ __forceinline__ void consume_tile_plain(const ConvParams& p, const Ti
                     float2 wa, wb;
                     noise_from_words2(ev ? q.a : v0, ev ? q.b : v1, ev ? v0 : q.c, ev ? v1 : q.d, p.noise_sc, wa,
                                       wb);
-                    out[r] = make_float2(__fadd_rn(out[r].x, wa.x), __fadd_rn(out[r].y, wa.y));
-                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, wb.x), __fadd_rn(out[r + 1].y, wb.y));
+                    out[r] = add_noise(out[r], wa);
+                    out[r + 1] = add_noise(out[r + 1], wb);
                 }
             } else if constexpr (R % 2 == 0) {
                 // odd tile base: every lane draws its own pair per row (rows two at a time)
@@ -529,8 +540,8 @@ __device__ __forceinline__ void consume_tile_plain(const ConvParams& p, const Ti
                     float2 w0, w1;
                     noise_from_words2(odd ? q0.c : q0.a, odd ? q0.d : q0.b, odd ? q1.c : q1.a, odd ? q1.d : q1.b,
                                       p.noise_sc, w0, w1);
-                    out[r] = make_float2(__fadd_rn(out[r].x, w0.x), __fadd_rn(out[r].y, w0.y));
-                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, w1.x), __fadd_rn(out[r + 1].y, w1.y));
+                    out[r] = add_noise(out[r], w0);
+                    out[r + 1] = add_noise(out[r + 1], w1);
                 }
             } else {
 #pragma unroll
@@ -541,7 +552,7 @@ __device__ __forceinline__ void consume_tile_plain(const ConvParams& p, const Ti
                                                   p.key0, p.key1);
                     const bool odd = (n & 1) != 0;
                     const float2 wv = noise_from_words(odd ? q.c : q.a, odd ? q.d : q.b, p.noise_sc);
-                    out[r] = make_float2(__fadd_rn(out[r].x, wv.x), __fadd_rn(out[r].y, wv.y));
+                    out[r] = add_noise(out[r], wv);
                 }
             }
         }
@@ -693,7 +704,7 @@ __device__ __forceinline__ void consume_body(const ConvParams& p, const TileInfo
         // epilogue: combine, add noise, store
         float2 out[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) out[r] = make_float2(__fsub_rn(A[r].x, B[r].y), __fadd_rn(A[r].y, B[r].x));
+        for (int r = 0; r < R; ++r) out[r] = combine(A[r], B[r]);
         if constexpr (NOISE) {
             const int64_t nb = p.t + ti.i0 + obase;  // global sample of row 0
             const uint32_t cg = static_cast<uint32_t>(p.chan_offset + ti.c);
@@ -713,8 +724,8 @@ __device__ __forceinline__ void consume_body(const ConvParams& p, const TileInfo
                     float2 wa, wb;
                     noise_from_words2(ev ? q.a : v0, ev ? q.b : v1, ev ? v0 : q.c, ev ? v1 : q.d, p.noise_sc, wa,
                                       wb);
-                    out[r] = make_float2(__fadd_rn(out[r].x, wa.x), __fadd_rn(out[r].y, wa.y));
-                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, wb.x), __fadd_rn(out[r + 1].y, wb.y));
+                    out[r] = add_noise(out[r], wa);
+                    out[r + 1] = add_noise(out[r + 1], wb);
                 }
             } else if constexpr (R % 2 == 0) {
                 // odd tile base: every lane draws its own pair per row (rows two at a time)
@@ -730,8 +741,8 @@ __device__ __forceinline__ void consume_body(const ConvParams& p, const TileInfo
                     float2 w0, w1;
                     noise_from_words2(odd ? q0.c : q0.a, odd ? q0.d : q0.b, odd ? q1.c : q1.a, odd ? q1.d : q1.b,
                                       p.noise_sc, w0, w1);
-                    out[r] = make_float2(__fadd_rn(out[r].x, w0.x), __fadd_rn(out[r].y, w0.y));
-                    out[r + 1] = make_float2(__fadd_rn(out[r + 1].x, w1.x), __fadd_rn(out[r + 1].y, w1.y));
+                    out[r] = add_noise(out[r], w0);
+                    out[r + 1] = add_noise(out[r + 1], w1);
                 }
             } else {
 #pragma unroll
@@ -742,7 +753,7 @@ __device__ __forceinline__ void consume_body(const ConvParams& p, const TileInfo
                                                   p.key0, p.key1);
                     const bool odd = (n & 1) != 0;
                     const float2 wv = noise_from_words(odd ? q.c : q.a, odd ? q.d : q.b, p.noise_sc);
-                    out[r] = make_float2(__fadd_rn(out[r].x, wv.x), __fadd_rn(out[r].y, wv.y));
+                    out[r] = add_noise(out[r], wv);
                 }
             }
         }

@@ -103,7 +103,9 @@ __device__ __forceinline__ float2 noise_from_words(uint32_t a, uint32_t b, float
 // Two samples at once, (a0, b0) and (a1, b1): the same operation sequence as
 // noise_from_words on each, with the floating-point steps packed into FFMA2 / FMUL2 /
 // FADD2 (per component exactly __fmaf_rn / __fmul_rn / __fadd_rn, so the results are
-// bit-identical) to halve their issue slots.
+// bit-identical) to halve their issue slots. ptxas contracts an FMUL2 that feeds an
+// FADD2 into one FFMA2 even with .rn; the two such pairs here (m - 1 and 1 - phi) have
+// exact products (scaling by a power of two), so the contraction does not change them.
 __device__ __forceinline__ void noise_from_words2(uint32_t a0, uint32_t b0, uint32_t a1, uint32_t b1, float sc,
                                                   float2& w0, float2& w1) {
     // radius: rho = sqrt(-2 ln u), u = ((a >> 8) + 1) 2^-24

@@ -140,6 +140,7 @@ struct tt_channel_s {
     size_t agg_scratch_elems = 0;
     float2* load_stage = nullptr;  // device staging for host-memory snapshot sources
     size_t load_stage_elems = 0;
+    cudaEvent_t ev_load = nullptr;  // the last loader kernel that read load_stage
     size_t dev_bytes = 0;
     Plan plan;
     // host-buffer path
@@ -761,6 +762,7 @@ void free_all(tt_channel_s* h) {
         if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
     }
     if (h->ev_start) cudaEventDestroy(h->ev_start);
+    if (h->ev_load) cudaEventDestroy(h->ev_load);
     for (int i = 0; i < 2; ++i) {
         if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
         if (h->cs_h2d[i]) cudaStreamDestroy(h->cs_h2d[i]);
@@ -927,13 +929,18 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
     const size_t elems = static_cast<size_t>(h->C) * count * h->L;
     const float2* src = reinterpret_cast<const float2*>(gains);
     if (!on_device) {
+        // the staging buffer is shared by every load of the handle: a load on another
+        // stream waits for the previous loader kernel to have read it
+        if (!h->ev_load) TT_CUDA(cudaEventCreateWithFlags(&h->ev_load, cudaEventDisableTiming), "event create");
         if (elems > h->load_stage_elems) {
-            TT_CUDA(cudaStreamSynchronize(st), "staging drain");
+            TT_CUDA(cudaEventSynchronize(h->ev_load), "staging drain");
             cudaFree(h->load_stage);
             h->load_stage = nullptr;
             h->load_stage_elems = 0;
             TT_CUDA(cudaMalloc(&h->load_stage, elems * sizeof(float2)), "cudaMalloc(snapshot staging)");
             h->load_stage_elems = elems;
+        } else {
+            TT_CUDA(cudaStreamWaitEvent(st, h->ev_load, 0), "stream wait");
         }
         TT_CUDA(cudaMemcpyAsync(h->load_stage, gains, elems * sizeof(float2), cudaMemcpyHostToDevice, st), "snapshot H2D");
         src = h->load_stage;
@@ -955,6 +962,7 @@ tt_status tt_channel_load_snapshots(tt_channel_t h, const float* gains, int64_t 
     tt::tt_load_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), 256, 0, st>>>(
         src, count, first_index, h->ring, h->cap, h->perm, h->C, h->L, fix_prev, fix_next);
     TT_CUDA(cudaGetLastError(), "snapshot loader launch");
+    if (!on_device) TT_CUDA(cudaEventRecord(h->ev_load, st), "event record");
     {
         // sparse rows follow the dense rows they are selected from (the previous row's
         // difference was just completed by fix_prev)

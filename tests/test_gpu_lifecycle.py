@@ -7,7 +7,8 @@
   to both resident neighbours (the interpolation through the reloaded block uses the
   new values on both sides);
 * the torch wrapper refuses tensors on the wrong device or of the wrong dtype;
-* a failed set_top_n leaves the handle dense with a dense plan.
+* a failed set_top_n leaves the handle dense with a dense plan;
+* host-memory snapshot loads on different streams do not race on the staging buffer.
 
 Every output is compared with the oracle on the same seeded inputs."""
 import numpy as np
@@ -202,3 +203,34 @@ def test_failed_set_top_n_leaves_a_dense_handle(cuda_device):
         ch.close()
     torch.cuda.empty_cache()
     compare(y, run.oracle(), "dense after a failed set_top_n")
+
+
+def test_host_loads_on_two_streams_share_the_staging_buffer(cuda_device):
+    """Snapshot loads from host memory go through one device staging buffer per handle.
+    Blocks loaded from host tensors on two streams back to back, with no host sync in
+    between: the second block's copy into the staging buffer must wait for the first
+    block's loader kernel (on the other stream) to have read it. Repeated with blocks of
+    decreasing size (the buffer is reused, not regrown)."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    w = ttsynth.get("c4").scaled(ues=64, n_per_call=4_000, calls=1)  # 128 channels, 48 taps, K = 17
+    run = Run(w, seed=21)
+    K = run.K
+    cuts = [0, 9, 14, K]  # blocks of 9, 5 and 3 snapshots
+    s1, s2 = torch.cuda.Stream(cuda_device), torch.cuda.Stream(cuda_device)
+    ch = Channel(run.delays, w.S, seed=run.seed, snapshot_capacity=K + 2, device=cuda_device)
+    try:
+        # a first, larger host load sizes the staging buffer for the blocks below
+        ch.load_snapshots(torch.zeros(run.C, K, w.L, 2), 0, stream=s1)
+        torch.cuda.synchronize()
+        for i in range(len(cuts) - 1):
+            blk = torch.from_numpy(np.ascontiguousarray(run.gains[:, cuts[i]:cuts[i + 1]]))  # CPU tensor: no wrapper sync
+            ch.load_snapshots(blk, cuts[i], stream=s1 if i % 2 == 0 else s2)
+        torch.cuda.synchronize()
+        y = _apply_all(ch, run, cuda_device)
+    finally:
+        ch.close()
+    ref = oracle.convolve(run.delays, w.S, run.gains, 0, run.x, 0, 0, run.N, sigma=run.sigma, seed=run.seed)
+    compare(y, ref, "host loads on two streams")

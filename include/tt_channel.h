@@ -119,7 +119,9 @@ tt_status tt_channel_create(tt_channel_t* out, int32_t num_ue, int32_t num_taps,
  * ("read time-varying CIR traces"; "discrete complex tap values over
  * time") into the ring. gains: float [C][count][L][2], host or device memory (the
  * library detects which); the copy is enqueued on `stream` and the source must stay
- * valid until it completes there. If the new block is contiguous with the resident
+ * valid until it completes there. A host source is staged through one device buffer
+ * owned by the handle; loads on different streams are ordered on that buffer (a
+ * load waits for the previous load's kernel to have read it). If the new block is contiguous with the resident
  * range the range grows (older snapshots fall out once capacity is exceeded);
  * otherwise the resident range is replaced by the new block. A block that starts
  * inside the resident range may also end inside it (a reload of snapshots already

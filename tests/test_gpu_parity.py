@@ -209,9 +209,11 @@ def test_kernels_bit_identical(cuda_device, monkeypatch, name, kw, calls):
     compare(outs["rw"], run.oracle(), name)
 
 
-@pytest.mark.parametrize("case", ["max_delay", "many_taps", "one_sample_calls", "unaligned_rows"])
+@pytest.mark.parametrize("case", ["max_delay", "many_taps", "max_taps", "duplicate_delays", "one_sample_calls",
+                                  "unaligned_rows"])
 def test_edge_cases(cuda_device, case):
-    """Edge cases of the boundary: the largest delay (TT_MAX_DELAY), very many taps,
+    """Edge cases of the boundary: the largest delay (TT_MAX_DELAY), very many taps and
+    the largest tap count (TT_MAX_TAPS), every tap at the same delay (duplicates add),
     1-sample calls (every call shorter than the delay line), and input / output rows
     that start 8 B off a 16-B boundary (the TMA staging splits off an 8-B head)."""
     import torch
@@ -225,6 +227,13 @@ def test_edge_cases(cuda_device, case):
     elif case == "many_taps":
         w = ttsynth.get("c2").scaled(ues=1, L=2000, D=4000, S=512, n_per_call=6_000, snr_db=10.0)
         calls = [6_000]
+    elif case == "max_taps":
+        w = ttsynth.get("c2").scaled(ues=1, L=4096, D=4096, S=256, n_per_call=1_500, snr_db=10.0)
+        calls = [700, 800]
+    elif case == "duplicate_delays":
+        w = ttsynth.get("c1").scaled(fixed_delays=(5,) * 8, fixed_pdp=(0.125,) * 8, L=8, D=5, S=100,
+                                     n_per_call=3_001)
+        calls = [1_000, 2_001]
     elif case == "one_sample_calls":
         w = ttsynth.get("c3").scaled(ues=1, dirs=2, n_per_call=40, calls=1)
         calls = [1] * 40
@@ -250,6 +259,34 @@ def test_edge_cases(cuda_device, case):
         ch.close()
         assert np.array_equal(y, run.gpu(cuda_device))
     compare(y, run.oracle(), case)
+
+
+def test_minimal_snapshot_capacity_streaming(cuda_device):
+    """snapshot_capacity = 2 (the minimum): each call covers one snapshot interval and the
+    next snapshot is loaded just before it, so the ring wraps every call; the streamed
+    output equals the oracle on the whole gain sequence."""
+    import torch
+
+    from paper_2601_08217_b200 import Channel
+
+    w = ttsynth.get("c4").scaled(ues=2, n_per_call=512, calls=8, S=512)
+    run = Run(w, seed=31)
+    assert run.K >= w.calls + 1
+    ch = Channel(run.delays, w.S, seed=run.seed, snapshot_capacity=2, device=cuda_device)
+    try:
+        ch.load_snapshots(torch.from_numpy(np.ascontiguousarray(run.gains[:, 0:2])).to(cuda_device), 0)
+        ys = []
+        for k in range(w.calls):
+            if k > 0:
+                ch.load_snapshots(torch.from_numpy(np.ascontiguousarray(run.gains[:, k + 1:k + 2])).to(cuda_device),
+                                  k + 1)
+            info = ch.info()
+            assert (info.resident_lo, info.resident_hi) == (k, k + 2)
+            xs = torch.from_numpy(np.ascontiguousarray(run.x[:, k * 512:(k + 1) * 512])).to(cuda_device)
+            ys.append(ch.apply(xs, noise_sigma=run.sigma).cpu().numpy())
+    finally:
+        ch.close()
+    compare(np.concatenate(ys, axis=1), run.oracle(), "capacity 2")
 
 
 def test_random_instances_vs_oracle(cuda_device):

@@ -22,7 +22,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("TT_PROF_DIR", os.path.join(ROOT, "profiles"))  # TT_PROF_DIR: summarise on the GPU box
 ROUND = os.environ.get("TT_ROUND", "r01")
 
 METRICS = [
